@@ -1,0 +1,182 @@
+/*
+ * mpsp.h - C ABI of libmpsp: multiple-precision CSR sparse matrix-vector
+ * multiplication on NVIDIA B200 (sm_100a).
+ *
+ * Operation (arXiv 1411.2377, PAPER.md:119-133 CSR storage of the nonzero
+ * elements; PAPER.md:182-186 the product A^(s,p) b; PAPER.md:282-284 (Fig. 4,
+ * BiCG) z = A p and z~ = A^T p~; BASELINE.json north_star for the rounding
+ * and order):
+ *
+ *     y_i = chain_i(A, x):  s = +0;  for k = rowptr[i] .. rowptr[i+1]-1
+ *                                     (ascending column index):
+ *                                 s = RN_p( s + RN_p( A_k * x[colidx[k]] ) )
+ *
+ * RN_p = round to nearest, ties to even, to p significant bits, after every
+ * multiply and every add (PAPER.md:84-85 lists RN among MPFR's modes; reading
+ * c1 in DESIGN.md).  A^T x uses the same chain over column j of A in
+ * ascending row index of A.  Results are bit-exact: every limb, exponent and
+ * sign is a pure function of (A, x), independent of launch configuration,
+ * binning and GPU count.
+ *
+ * VALUE ENCODING (packed host/device format):
+ *   A nonzero value is (-1)^sign * (M / 2^p) * 2^exp with 2^(p-1) <= M < 2^p
+ *   (MPFR convention).  M is stored as L = p/32 uint32 limbs, limb 0 least
+ *   significant, so the MSB of limb L-1 is set.  exp is int32, sign is uint8
+ *   in {0,1}.  Zero is "all limbs 0" (its exp and sign are ignored on input;
+ *   written as exp 0, sign 0 on output; no -0 is ever produced).  There is no
+ *   NaN/Inf/subnormal.  Input exponents must satisfy |exp| <= 2^29, which
+ *   makes int32 overflow impossible inside the chain.
+ *
+ * Element layouts: limbs arrays are element-major ("AoS"): element i's limbs
+ * are limbs[i*L .. i*L+L-1].  exps/signs are one entry per element.
+ *
+ * THREAD SAFETY: one handle per host thread at a time; distinct handles are
+ * independent.  All functions return MPSP_OK (0) or a negative error code.
+ */
+#ifndef MPSP_H
+#define MPSP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes ------------------------------------------------------ */
+#define MPSP_OK            0
+#define MPSP_E_ARG        -1   /* null pointer, n < 0, bad row range, misaligned */
+#define MPSP_E_PREC       -2   /* p % 32 != 0 or p outside the supported set */
+#define MPSP_E_CSR        -3   /* rowptr[0]!=0, non-monotone, rowptr[n] > 2^31-1,
+                                  colidx outside [0, n) */
+#define MPSP_E_UNSORTED   -4   /* colidx not strictly increasing within a row
+                                  (covers duplicates); the library does not sort */
+#define MPSP_E_VALUE      -5   /* nonzero value without MSB of limb L-1 set,
+                                  or |exp| > 2^29 */
+#define MPSP_E_NOMEM      -6   /* host or device allocation failed */
+#define MPSP_E_CUDA       -7   /* CUDA runtime error (see mpsp_strerror / mpsp_last_cuda_error) */
+#define MPSP_E_ALIAS      -8   /* x and y storage overlap */
+#define MPSP_E_DEVICE     -9   /* current device (or a pointer's device) differs from the handle's */
+#define MPSP_E_NOTRANS   -10   /* spmv_t on a handle built without MPSP_WITH_TRANSPOSE */
+
+/* ---- flags for mpsp_csr_create ---------------------------------------- */
+#define MPSP_WITH_TRANSPOSE  0x1u  /* also build rows [row_begin,row_end) of A^T */
+
+typedef struct mpsp_csr mpsp_csr;
+
+/*
+ * mpsp_csr_create - validate a CSR matrix and build its device form.
+ *
+ *   out        receives the handle (NULL on error; nothing leaks on error).
+ *   p_bits     precision p in bits; supported: 32, 64, 128, 256, 512, 1024
+ *              (L = p/32 in {1,2,4,8,16,32}).
+ *   n          A is n x n (n >= 0).
+ *   rowptr     host int64[n+1]: CSR row pointers (rowptr[0] = 0, monotone).
+ *   colidx     host int32[nnz], nnz = rowptr[n] <= 2^31-1; strictly
+ *              increasing within each row, values in [0, n).
+ *   limbs      host uint32[nnz*L] element-major mantissas (see encoding).
+ *   exps       host int32[nnz]; signs host uint8[nnz].
+ *   row_begin, row_end
+ *              the handle computes rows [row_begin, row_end) of y (and, with
+ *              MPSP_WITH_TRANSPOSE, of A^T x).  0 <= row_begin <= row_end <= n.
+ *              Single GPU: 0, n.  Row-block multi-GPU: one block per rank.
+ *   flags      MPSP_WITH_TRANSPOSE or 0.
+ *
+ * The full global CSR is passed in host memory; the handle copies what it
+ * needs (the caller may free or modify the inputs on return) and owns all
+ * device memory, allocated on the CURRENT CUDA device.  Explicit zero entries
+ * are kept (they contribute +0).  One-off cost: O(nnz*L) host work plus one
+ * host-to-device copy; it synchronises the device before returning.
+ *
+ * Errors: MPSP_E_ARG, MPSP_E_PREC, MPSP_E_CSR, MPSP_E_UNSORTED, MPSP_E_VALUE,
+ * MPSP_E_NOMEM, MPSP_E_CUDA.
+ */
+int mpsp_csr_create(mpsp_csr **out, int p_bits, int64_t n,
+                    const int64_t *rowptr, const int32_t *colidx,
+                    const uint32_t *limbs, const int32_t *exps, const uint8_t *signs,
+                    int64_t row_begin, int64_t row_end, uint32_t flags);
+
+/*
+ * mpsp_spmv - y[i - row_begin] = chain_i(A, x) for i in [row_begin, row_end).
+ *
+ * All pointers are DEVICE pointers on the handle's device:
+ *   x_limbs uint32[n*L], x_exps int32[n], x_signs uint8[n]   (the full x)
+ *   y_limbs uint32[r*L], y_exps int32[r], y_signs uint8[r]   (r = row_end-row_begin)
+ * limbs pointers must be aligned to min(16, 4L) bytes.  x and y must not
+ * overlap.  Pointers to empty arrays (n = 0, or an empty row range) may be
+ * NULL.  The work is enqueued on `cuda_stream` (a cudaStream_t; NULL =
+ * legacy default stream) and the call returns without synchronising; x and y
+ * are caller-owned and must stay alive until the stream work completes.
+ * x contents are not validated (an unnormalised nonzero x is undefined
+ * behaviour) unless the environment variable MPSP_VALIDATE=1 is set.
+ *
+ * Errors: MPSP_E_ARG, MPSP_E_ALIAS, MPSP_E_DEVICE, MPSP_E_VALUE (validation
+ * mode only), MPSP_E_CUDA (launch failure).
+ */
+int mpsp_spmv(const mpsp_csr *A,
+              const uint32_t *x_limbs, const int32_t *x_exps, const uint8_t *x_signs,
+              uint32_t *y_limbs, int32_t *y_exps, uint8_t *y_signs, void *cuda_stream);
+
+/*
+ * mpsp_spmv_t - y[j - row_begin] = chainT_j(A, x): over i ascending with
+ * (i, j) stored, s = RN(s + RN(A_ij * x_i)), for j in [row_begin, row_end).
+ * Same arguments and errors as mpsp_spmv, plus MPSP_E_NOTRANS.
+ */
+int mpsp_spmv_t(const mpsp_csr *A,
+                const uint32_t *x_limbs, const int32_t *x_exps, const uint8_t *x_signs,
+                uint32_t *y_limbs, int32_t *y_exps, uint8_t *y_signs, void *cuda_stream);
+
+/*
+ * mpsp_spmv_host / mpsp_spmv_t_host - the same operations on HOST buffers
+ * (pageable or pinned).  Copies x to a device workspace owned by the handle,
+ * runs the kernel on the handle's internal stream, copies y back and
+ * synchronises before returning.  Same errors as the device variants
+ * (MPSP_E_ALIAS is checked on the host ranges).
+ */
+int mpsp_spmv_host(mpsp_csr *A,
+                   const uint32_t *x_limbs, const int32_t *x_exps, const uint8_t *x_signs,
+                   uint32_t *y_limbs, int32_t *y_exps, uint8_t *y_signs);
+int mpsp_spmv_t_host(mpsp_csr *A,
+                     const uint32_t *x_limbs, const int32_t *x_exps, const uint8_t *x_signs,
+                     uint32_t *y_limbs, int32_t *y_exps, uint8_t *y_signs);
+
+/* mpsp_destroy - synchronise the handle's device and free everything. NULL-safe. */
+void mpsp_destroy(mpsp_csr *A);
+
+/* mpsp_strerror - static, library-owned description of an error code. */
+const char *mpsp_strerror(int code);
+
+/* Text of the last CUDA error seen by this thread (static storage). */
+const char *mpsp_last_cuda_error(void);
+
+/*
+ * mpsp_csr_info - sizes of a handle, for bindings and reporting.
+ *   info[0] = p_bits, info[1] = n, info[2] = row_begin, info[3] = row_end,
+ *   info[4] = nnz of the row block of A, info[5] = nnz of the row block of A^T
+ *   (-1 without transpose), info[6] = device bytes owned by the handle,
+ *   info[7] = device ordinal, info[8] = stored slots of A incl. padding,
+ *   info[9] = max row length in the block of A.
+ * Errors: MPSP_E_ARG.
+ */
+int mpsp_csr_info(const mpsp_csr *A, int64_t info[10]);
+
+/* Number of kernels this library has launched in this process (monotone). */
+int64_t mpsp_launch_count(void);
+
+/*
+ * mpsp_imad_bench - measures the sustained 32x32->64 limb-MAC rate of the
+ * current device with the same Comba (product-scanning) instruction pattern
+ * the SpMV kernels use (IMAD.WIDE.U32 with carry-out), all SMs busy.
+ *   out[0] = limb-MACs per second, out[1] = kernel seconds, out[2] = SM count.
+ * The roofline denominator for the integer-bound configurations.
+ * Errors: MPSP_E_CUDA.
+ */
+int mpsp_imad_bench(double out[3]);
+
+/* Supported precisions query: returns 1 if p_bits is supported, else 0. */
+int mpsp_supported_precision(int p_bits);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MPSP_H */

@@ -1,0 +1,158 @@
+"""Python face of the C ABI: CSR handles and device MP vectors.
+
+Argument marshalling only - every step of the SpMV runs in libmpsp's CUDA
+kernels.  torch provides device memory and streams (plumbing).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+try:
+    import torch
+except ImportError:  # pragma: no cover
+    torch = None
+
+
+def _ptr(a) -> int:
+    if a is None:
+        return 0
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()
+
+
+@dataclass
+class MPVec:
+    """A p-bit vector on the GPU: limbs int32 [n, L] (uint32 bit patterns),
+    exps int32 [n], signs uint8 [n].  Packed format of include/mpsp.h."""
+    limbs: "torch.Tensor"
+    exps: "torch.Tensor"
+    signs: "torch.Tensor"
+
+    @property
+    def n(self) -> int:
+        return int(self.exps.shape[0])
+
+    @property
+    def L(self) -> int:
+        return int(self.limbs.shape[1])
+
+    @classmethod
+    def empty(cls, n: int, L: int, device="cuda") -> "MPVec":
+        return cls(torch.empty((n, L), dtype=torch.int32, device=device),
+                   torch.empty((n,), dtype=torch.int32, device=device),
+                   torch.empty((n,), dtype=torch.uint8, device=device))
+
+    @classmethod
+    def from_host(cls, limbs: np.ndarray, exps: np.ndarray, signs: np.ndarray, device="cuda",
+                  L: int | None = None) -> "MPVec":
+        L = L or (limbs.shape[1] if limbs.ndim == 2 else None)
+        l = np.ascontiguousarray(limbs, dtype=np.uint32).reshape(-1, L).view(np.int32)
+        return cls(torch.from_numpy(l.copy()).to(device),
+                   torch.from_numpy(np.ascontiguousarray(exps, dtype=np.int32).copy()).to(device),
+                   torch.from_numpy(np.ascontiguousarray(signs, dtype=np.uint8).copy()).to(device))
+
+    def to_host(self):
+        l = self.limbs.cpu().numpy().view(np.uint32)
+        return l, self.exps.cpu().numpy(), self.signs.cpu().numpy()
+
+
+class CSR:
+    """Handle on rows [row_begin, row_end) of an n x n p-bit CSR matrix on the
+    current CUDA device (mpsp_csr_create).  Inputs are host numpy arrays in
+    the packed format; the handle copies them."""
+
+    def __init__(self, p: int, rowptr, colidx, limbs, exps, signs, rows=None,
+                 transpose: bool = False):
+        self.p = int(p)
+        self.L = self.p // 32
+        self.n = int(len(rowptr) - 1)
+        rb, re = (0, self.n) if rows is None else (int(rows[0]), int(rows[1]))
+        self.row_begin, self.row_end = rb, re
+        self._keep = [np.ascontiguousarray(rowptr, dtype=np.int64),
+                      np.ascontiguousarray(colidx, dtype=np.int32),
+                      np.ascontiguousarray(limbs, dtype=np.uint32),
+                      np.ascontiguousarray(exps, dtype=np.int32),
+                      np.ascontiguousarray(signs, dtype=np.uint8)]
+        rp, ci, li, ex, sg = self._keep
+        h = ctypes.c_void_p()
+        rc = _lib.lib().mpsp_csr_create(ctypes.byref(h), self.p, self.n, _ptr(rp), _ptr(ci),
+                                        _ptr(li), _ptr(ex), _ptr(sg), rb, re,
+                                        _lib.MPSP_WITH_TRANSPOSE if transpose else 0)
+        self._keep = None
+        _lib.check(rc, "mpsp_csr_create")
+        self._h = h
+        self.transpose = transpose
+
+    @property
+    def rows(self) -> int:
+        return self.row_end - self.row_begin
+
+    def info(self) -> dict:
+        arr = (ctypes.c_int64 * 10)()
+        _lib.check(_lib.lib().mpsp_csr_info(self._h, arr), "mpsp_csr_info")
+        keys = ("p", "n", "row_begin", "row_end", "nnz", "nnz_t", "device_bytes", "device",
+                "slots", "max_row")
+        return dict(zip(keys, [int(v) for v in arr]))
+
+    def _apply(self, fn, x: MPVec, out: MPVec | None, stream) -> MPVec:
+        if out is None:
+            out = MPVec.empty(self.rows, self.L, device=x.limbs.device)
+        if stream is None:
+            stream = torch.cuda.current_stream(x.limbs.device).cuda_stream
+        elif hasattr(stream, "cuda_stream"):
+            stream = stream.cuda_stream
+        rc = fn(self._h, _ptr(x.limbs), _ptr(x.exps), _ptr(x.signs),
+                _ptr(out.limbs), _ptr(out.exps), _ptr(out.signs), ctypes.c_void_p(stream))
+        _lib.check(rc, fn.__name__)
+        return out
+
+    def spmv(self, x: MPVec, out: MPVec | None = None, stream=None) -> MPVec:
+        """y = A x for the handle's rows (async on `stream`, default: torch's current)."""
+        return self._apply(_lib.lib().mpsp_spmv, x, out, stream)
+
+    def spmv_t(self, x: MPVec, out: MPVec | None = None, stream=None) -> MPVec:
+        """y = A^T x for the handle's rows of A^T (needs transpose=True)."""
+        return self._apply(_lib.lib().mpsp_spmv_t, x, out, stream)
+
+    def _host(self, fn, xl, xe, xs, out=None):
+        xl = np.ascontiguousarray(xl, dtype=np.uint32)
+        xe = np.ascontiguousarray(xe, dtype=np.int32)
+        xs = np.ascontiguousarray(xs, dtype=np.uint8)
+        if out is None:
+            out = (np.empty((self.rows, self.L), np.uint32), np.empty(self.rows, np.int32),
+                   np.empty(self.rows, np.uint8))
+        yl, ye, ys = out
+        rc = fn(self._h, _ptr(xl), _ptr(xe), _ptr(xs), _ptr(yl), _ptr(ye), _ptr(ys))
+        _lib.check(rc, fn.__name__)
+        return out
+
+    def spmv_host(self, xl, xe, xs, out=None):
+        """y = A x with HOST buffers (copies inside the call; synchronous)."""
+        return self._host(_lib.lib().mpsp_spmv_host, xl, xe, xs, out)
+
+    def spmv_t_host(self, xl, xe, xs, out=None):
+        return self._host(_lib.lib().mpsp_spmv_t_host, xl, xe, xs, out)
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.lib().mpsp_destroy(h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

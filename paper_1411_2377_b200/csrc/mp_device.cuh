@@ -1,0 +1,241 @@
+// mp_device.cuh - p-bit binary floating-point arithmetic with round-to-
+// nearest-even, as sm_100a device functions.  L = p/32 uint32 limbs.
+//
+// Semantics (BASELINE.json north_star):
+//   value = (-1)^s * M/2^p * 2^e,  2^(p-1) <= M < 2^p, zero <=> M == 0.
+//   mp_mul: t = RN(a * x)        (exact 2L-limb product, one rounding)
+//   mp_add: s = RN(s + t)        (exact alignment with a guard limb + sticky,
+//                                 one rounding; exact zero -> +0)
+// Everything is held in registers; all limb loops are fully unrolled so the
+// arrays never touch local memory.  Shares no code with the CPU reference.
+#pragma once
+#include <cstdint>
+
+namespace mpsp {
+
+// --------------------------------------------------------------------------
+// Comba multiply-accumulate step: (c2:c1:c0) += a*b.  ptxas fuses the
+// mad.lo.cc / madc.hi.cc pair into one IMAD.WIDE.U32 with a carry-out
+// predicate, and pairs of carries into one IADD3.X.
+// --------------------------------------------------------------------------
+__device__ __forceinline__ void mac3(uint32_t& c0, uint32_t& c1, uint32_t& c2,
+                                     uint32_t a, uint32_t b) {
+  asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
+      "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
+      "addc.u32 %2, %2, 0;"
+      : "+r"(c0), "+r"(c1), "+r"(c2)
+      : "r"(a), "r"(b));
+}
+
+// Register-resident MP number.  m[L-1] == 0 <=> zero.
+template <int L>
+struct MP {
+  uint32_t m[L];
+  int32_t e;
+  uint32_t s;
+  __device__ __forceinline__ bool is_zero() const { return m[L - 1] == 0u; }
+  __device__ __forceinline__ void set_zero() {
+#pragma unroll
+    for (int i = 0; i < L; ++i) m[i] = 0u;
+    e = 0;
+    s = 0u;
+  }
+};
+
+// Round-to-nearest-even increment of an L-limb mantissa given round bit and
+// sticky.  Returns the carry out of the top limb (mantissa became 2^p; the
+// caller renormalises to 2^(p-1) and bumps the exponent).
+template <int L>
+__device__ __forceinline__ uint32_t rne_increment(uint32_t (&m)[L], uint32_t rb, uint32_t sticky) {
+  uint32_t c = rb & ((sticky != 0u) | (m[0] & 1u));
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    uint64_t t = (uint64_t)m[i] + c;
+    m[i] = (uint32_t)t;
+    c = (uint32_t)(t >> 32);
+  }
+  return c;
+}
+
+// --------------------------------------------------------------------------
+// t = RN_p(a * x).  a, x: L-limb mantissas (zero allowed: result zero).
+// Exponent of the result: ea + ex (top product bit set) or ea + ex - 1,
+// +1 if rounding carried out.
+// --------------------------------------------------------------------------
+template <int L>
+__device__ __forceinline__ void mp_mul(const uint32_t (&a)[L], int32_t ea, uint32_t sa,
+                                       const uint32_t (&x)[L], int32_t ex, uint32_t sx,
+                                       MP<L>& t) {
+  uint32_t c0 = 0u, c1 = 0u, c2 = 0u;
+  uint32_t sticky = 0u, w = 0u;
+  uint32_t P[L];
+#pragma unroll
+  for (int k = 0; k < 2 * L - 1; ++k) {
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      const int j = k - i;
+      if (j < 0 || j >= L) continue;
+      mac3(c0, c1, c2, a[i], x[j]);
+    }
+    if (k < L - 1) sticky |= c0;           // columns 0..L-2: only "nonzero?" matters
+    else if (k == L - 1) w = c0;           // limb L-1: round bit(s) + sticky
+    else P[k - L] = c0;                    // limbs L..2L-2 of the product
+    c0 = c1; c1 = c2; c2 = 0u;
+  }
+  P[L - 1] = c0;                           // limb 2L-1
+  const bool top = (P[L - 1] >> 31) != 0u;
+  uint32_t rb, st;
+  if (top) {
+#pragma unroll
+    for (int i = 0; i < L; ++i) t.m[i] = P[i];
+    rb = w >> 31;
+    st = sticky | (w << 1);
+  } else {
+#pragma unroll
+    for (int i = L - 1; i > 0; --i) t.m[i] = __funnelshift_l(P[i - 1], P[i], 1);
+    t.m[0] = __funnelshift_l(w, P[0], 1);
+    rb = (w >> 30) & 1u;
+    st = sticky | (w << 2);
+  }
+  const uint32_t cy = rne_increment<L>(t.m, rb, st);
+  if (cy) t.m[L - 1] = 0x80000000u;
+  t.e = ea + ex - (top ? 0 : 1) + (int32_t)cy;
+  t.s = sa ^ sx;
+}
+
+// --------------------------------------------------------------------------
+// Variable shifts over N-limb register arrays (binary decomposition of the
+// limb count so indices stay compile-time; no local memory).
+// --------------------------------------------------------------------------
+template <int N>
+__device__ __forceinline__ void shr_bits_sticky(uint32_t (&v)[N], uint32_t d, uint32_t& sticky) {
+  const uint32_t q = d >> 5, r = d & 31u;
+#pragma unroll
+  for (int b = 1; b < N; b <<= 1) {
+    const bool on = (q & (uint32_t)b) != 0u;
+    uint32_t drop = 0u;
+#pragma unroll
+    for (int i = 0; i < b; ++i) drop |= v[i];
+    sticky |= on ? drop : 0u;
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = on ? (i + b < N ? v[i + b] : 0u) : v[i];
+  }
+  sticky |= r ? (v[0] << (32u - r)) : 0u;
+#pragma unroll
+  for (int i = 0; i < N - 1; ++i) v[i] = __funnelshift_r(v[i], v[i + 1], r);
+  v[N - 1] >>= r;
+}
+
+template <int N>
+__device__ __forceinline__ void shl_bits(uint32_t (&v)[N], uint32_t d) {
+  const uint32_t q = d >> 5, r = d & 31u;
+#pragma unroll
+  for (int b = 1; b < N; b <<= 1) {
+    const bool on = (q & (uint32_t)b) != 0u;
+#pragma unroll
+    for (int i = N - 1; i >= 0; --i) v[i] = on ? (i - b >= 0 ? v[i - b] : 0u) : v[i];
+  }
+#pragma unroll
+  for (int i = N - 1; i > 0; --i) v[i] = __funnelshift_l(v[i - 1], v[i], r);
+  v[0] <<= r;
+}
+
+template <int N>
+__device__ __forceinline__ uint32_t clz_limbs(const uint32_t (&v)[N]) {
+  uint32_t lz = 0u;
+  bool found = false;
+#pragma unroll
+  for (int i = N - 1; i >= 0; --i) {
+    const uint32_t c = __clz(v[i]);
+    lz += found ? 0u : c;
+    found = found || (v[i] != 0u);
+  }
+  return lz;
+}
+
+// --------------------------------------------------------------------------
+// s = RN_p(s + t)   (the oracle's add() computes the
+// same value by exact integer alignment).  Working width: L+1 limbs, i.e.
+// one 32-bit guard limb below the LSB, plus a sticky word for bits shifted
+// beyond it.  |exponent gap| >= p+2 returns the larger operand (far-path
+// lemma).
+// --------------------------------------------------------------------------
+template <int L>
+__device__ __forceinline__ void mp_add(MP<L>& s, const MP<L>& t) {
+  if (t.is_zero()) return;
+  if (s.is_zero()) { s = t; return; }
+  // |t| > |s| ?  compare (e, M)
+  uint32_t borrow = 0u;
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    uint64_t dd = (uint64_t)s.m[i] - t.m[i] - borrow;
+    borrow = (uint32_t)(dd >> 63);
+  }
+  const bool t_big = (t.e > s.e) || (t.e == s.e && borrow);
+  uint32_t X[L + 1], Y[L + 1];
+  X[0] = 0u;
+  Y[0] = 0u;
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    X[i + 1] = t_big ? t.m[i] : s.m[i];
+    Y[i + 1] = t_big ? s.m[i] : t.m[i];
+  }
+  const int32_t eb = t_big ? t.e : s.e;
+  const int32_t esm = t_big ? s.e : t.e;
+  const uint32_t sb = t_big ? t.s : s.s;
+  const bool same = (t.s == s.s);
+  const uint32_t d = (uint32_t)eb - (uint32_t)esm;      // exact as uint32
+  if (d >= (uint32_t)(32 * L + 2)) {                    // far-path lemma
+    if (t_big) s = t;
+    return;
+  }
+  uint32_t stk = 0u;
+  shr_bits_sticky<L + 1>(Y, d, stk);
+  uint32_t Z[L + 1];
+  int32_t e;
+  uint32_t rb, st;
+  if (same) {
+    uint32_t c = 0u;
+#pragma unroll
+    for (int i = 0; i <= L; ++i) {
+      uint64_t tt = (uint64_t)X[i] + Y[i] + c;
+      Z[i] = (uint32_t)tt;
+      c = (uint32_t)(tt >> 32);
+    }
+    if (c) {                                             // shift right by 1
+      const uint32_t lost = Z[0] & 1u;
+#pragma unroll
+      for (int i = 0; i < L; ++i) Z[i] = __funnelshift_r(Z[i], Z[i + 1], 1);
+      Z[L] = (Z[L] >> 1) | 0x80000000u;
+      stk |= lost;
+      e = eb + 1;
+    } else {
+      e = eb;
+    }
+  } else {
+    uint32_t bw = stk != 0u ? 1u : 0u;                 // X - Y - [sticky]
+#pragma unroll
+    for (int i = 0; i <= L; ++i) {
+      uint64_t tt = (uint64_t)X[i] - Y[i] - bw;
+      Z[i] = (uint32_t)tt;
+      bw = (uint32_t)(tt >> 63);
+    }
+    uint32_t any = 0u;
+#pragma unroll
+    for (int i = 0; i <= L; ++i) any |= Z[i];
+    if (any == 0u) { s.set_zero(); return; }            // exact cancellation: +0
+    const uint32_t lz = clz_limbs<L + 1>(Z);
+    shl_bits<L + 1>(Z, lz);
+    e = eb - (int32_t)lz;
+  }
+  rb = Z[0] >> 31;
+  st = stk | (Z[0] << 1);
+#pragma unroll
+  for (int i = 0; i < L; ++i) s.m[i] = Z[i + 1];
+  const uint32_t cy = rne_increment<L>(s.m, rb, st);
+  if (cy) s.m[L - 1] = 0x80000000u;
+  s.e = e + (int32_t)cy;
+  s.s = sb;
+}
+
+}  // namespace mpsp

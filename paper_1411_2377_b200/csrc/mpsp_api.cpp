@@ -1,0 +1,512 @@
+// mpsp_api.cpp - the C ABI of include/mpsp.h: validation, transpose, row
+// binning / SELL repack, device upload, argument checks and launches.
+//
+// Host side of SURVEY.md 8(a) rows a1-a3 (one-off, outside the timed loop):
+//   a1 validate + pack: CSR invariants, value encodings
+//      (MSB set, |exp| <= 2^29), limbs repacked into the chunk-major SELL
+//      layout of layout.h, sign packed into the exponent word.
+//   a2 transpose: stable counting sort on column -> ascending row index of A
+//      inside each transposed row (BASELINE.json north_star (3)).
+//   a3 binning: rows sorted by length (descending, stable) into slices of 32.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <thread>
+#include <vector>
+
+#include "../../include/mpsp.h"
+#include "layout.h"
+
+using namespace mpsp;
+
+namespace {
+
+thread_local char g_cuda_err[256] = "no error";
+
+int cuda_fail(cudaError_t e) {
+  std::snprintf(g_cuda_err, sizeof g_cuda_err, "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+  cudaGetLastError();  // clear sticky-free errors
+  return MPSP_E_CUDA;
+}
+
+template <class F>
+void parallel_for(int64_t n, F f) {
+  unsigned hw = std::thread::hardware_concurrency();
+  int64_t nt = std::max<int64_t>(1, std::min<int64_t>(hw ? hw : 1, 32));
+  if (n < (1 << 16)) nt = 1;
+  if (nt == 1) { f(0, n); return; }
+  std::vector<std::thread> th;
+  const int64_t chunk = (n + nt - 1) / nt;
+  for (int64_t t = 0; t < nt; ++t) {
+    int64_t b = t * chunk, e = std::min(n, b + chunk);
+    if (b >= e) break;
+    th.emplace_back([=] { f(b, e); });
+  }
+  for (auto& x : th) x.join();
+}
+
+struct DevPart {
+  int64_t nrows = 0, nnz = 0, nslices = 0, nentries = 0;
+  int32_t max_len = 0;
+  int64_t* slice_ptr = nullptr;
+  int32_t* slot_row = nullptr;
+  int32_t* slot_len = nullptr;
+  int32_t* col = nullptr;
+  int32_t* expw = nullptr;
+  uint32_t* limbs = nullptr;
+  size_t bytes = 0;
+
+  PartView view() const {
+    PartView v;
+    v.slice_ptr = slice_ptr; v.slot_row = slot_row; v.slot_len = slot_len;
+    v.col = col; v.expw = expw; v.limbs = limbs;
+    v.nslices = nslices; v.nslots = nslices * 32;
+    return v;
+  }
+  void release() {
+    cudaFree(slice_ptr); cudaFree(slot_row); cudaFree(slot_len);
+    cudaFree(col); cudaFree(expw); cudaFree(limbs);
+    slice_ptr = nullptr; slot_row = nullptr; slot_len = nullptr;
+    col = nullptr; expw = nullptr; limbs = nullptr;
+  }
+};
+
+}  // namespace
+
+struct mpsp_csr {
+  int dev = 0;
+  int p = 0, L = 0;
+  int64_t n = 0, rb = 0, re = 0;
+  uint32_t flags = 0;
+  bool has_t = false;
+  DevPart A, T;
+  // host-buffer API workspace (lazily allocated)
+  cudaStream_t stream = nullptr;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+};
+
+namespace {
+
+bool supported_L(int L) { return L == 1 || L == 2 || L == 4 || L == 8 || L == 16 || L == 32; }
+
+// Build one part (rows [0,nrows) of a local CSR whose entry e of local row r
+// is source entry src(r, e)).
+//   lrp : local rowptr (int64, nrows+1), entries in order (ascending column)
+//   lcol: local column of entry e
+//   srck: source index k into (limbs, exps, signs) of entry e (or nullptr:
+//         k = k0 + e)
+template <class Dummy = void>
+int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32_t* lcol,
+               const int64_t* srck, int64_t k0, const uint32_t* limbs, const int32_t* exps,
+               const uint8_t* signs) {
+  P.nrows = nrows;
+  P.nnz = lrp[nrows] - lrp[0];
+  // --- a3: stable counting sort of rows by length, descending
+  int32_t maxlen = 0;
+  for (int64_t r = 0; r < nrows; ++r) maxlen = std::max<int32_t>(maxlen, (int32_t)(lrp[r + 1] - lrp[r]));
+  P.max_len = maxlen;
+  std::vector<int64_t> cnt((size_t)maxlen + 2, 0);
+  for (int64_t r = 0; r < nrows; ++r) cnt[(size_t)(maxlen - (lrp[r + 1] - lrp[r]))]++;
+  int64_t acc = 0;
+  for (auto& c : cnt) { int64_t t = c; c = acc; acc += t; }
+  std::vector<int32_t> order((size_t)nrows);
+  for (int64_t r = 0; r < nrows; ++r) order[(size_t)cnt[(size_t)(maxlen - (lrp[r + 1] - lrp[r]))]++] = (int32_t)r;
+  const int64_t nslices = (nrows + 31) / 32;
+  P.nslices = nslices;
+  std::vector<int64_t> sp((size_t)nslices + 1, 0);
+  std::vector<int32_t> srow((size_t)nslices * 32, -1), slen((size_t)nslices * 32, 0);
+  for (int64_t s = 0; s < nslices; ++s) {
+    int64_t w = 0;
+    for (int l = 0; l < 32; ++l) {
+      int64_t slot = s * 32 + l;
+      if (slot < nrows) {
+        int32_t r = order[(size_t)slot];
+        srow[(size_t)slot] = r;
+        slen[(size_t)slot] = (int32_t)(lrp[r + 1] - lrp[r]);
+        w = std::max<int64_t>(w, slen[(size_t)slot]);
+      }
+    }
+    sp[(size_t)s + 1] = sp[(size_t)s] + 32 * w;
+  }
+  const int64_t nent = sp[(size_t)nslices];
+  P.nentries = nent;
+  const int CW = L < 4 ? L : 4, NC = L / CW;
+  // --- a1: repack (host), zero-filled padding
+  std::vector<int32_t> hcol, hexp;
+  std::vector<uint32_t> hl;
+  try {
+    hcol.assign((size_t)nent, 0);
+    hexp.assign((size_t)nent, 0);
+    hl.assign((size_t)nent * (size_t)L, 0u);
+  } catch (const std::bad_alloc&) {
+    return MPSP_E_NOMEM;
+  }
+  parallel_for(nslices, [&](int64_t s0, int64_t s1) {
+    for (int64_t s = s0; s < s1; ++s) {
+      for (int l = 0; l < 32; ++l) {
+        const int64_t slot = s * 32 + l;
+        const int32_t r = srow[(size_t)slot];
+        if (r < 0) continue;
+        const int64_t len = slen[(size_t)slot];
+        for (int64_t j = 0; j < len; ++j) {
+          const int64_t e = lrp[r] + j;                 // local entry
+          const int64_t k = srck ? srck[e] : k0 + e;    // source entry
+          const int64_t g = sp[(size_t)s] / 32 + j;
+          const int64_t E = g * 32 + l;
+          hcol[(size_t)E] = lcol[e];
+          const uint32_t* src = limbs + (size_t)k * L;
+          bool nz = src[L - 1] != 0u;
+          hexp[(size_t)E] = nz ? (int32_t)(((uint32_t)signs[k] << 31) | ((uint32_t)exps[k] & 0x7fffffffu)) : 0;
+          for (int c = 0; c < NC; ++c)
+            for (int w = 0; w < CW; ++w)
+              hl[(size_t)(((g * NC + c) * 32 + l) * CW + w)] = nz ? src[c * CW + w] : 0u;
+        }
+      }
+    }
+  });
+  // --- upload
+  auto up = [&](void** dst, const void* src, size_t bytes) -> int {
+    if (bytes == 0) bytes = 16;  // keep pointers valid for empty parts
+    cudaError_t e = cudaMalloc(dst, bytes);
+    if (e != cudaSuccess) { cudaGetLastError(); return e == cudaErrorMemoryAllocation ? MPSP_E_NOMEM : cuda_fail(e); }
+    P.bytes += bytes;
+    if (src) {
+      e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return cuda_fail(e);
+    }
+    return MPSP_OK;
+  };
+  int rc;
+  if ((rc = up((void**)&P.slice_ptr, sp.data(), sp.size() * 8)) ||
+      (rc = up((void**)&P.slot_row, srow.data(), srow.size() * 4)) ||
+      (rc = up((void**)&P.slot_len, slen.data(), slen.size() * 4)) ||
+      (rc = up((void**)&P.col, hcol.data(), hcol.size() * 4)) ||
+      (rc = up((void**)&P.expw, hexp.data(), hexp.size() * 4)) ||
+      (rc = up((void**)&P.limbs, hl.data(), hl.size() * 4)))
+    return rc;
+  return MPSP_OK;
+}
+
+bool env_validate() {
+  const char* v = std::getenv("MPSP_VALIDATE");
+  return v && v[0] == '1';
+}
+
+bool overlap(const void* a, size_t na, const void* b, size_t nb) {
+  if (!a || !b || !na || !nb) return false;
+  const char* pa = (const char*)a;
+  const char* pb = (const char*)b;
+  return pa < pb + nb && pb < pa + na;
+}
+
+int check_device_ptr(const void* p, int dev) {
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) { cudaGetLastError(); return MPSP_E_ARG; }
+  if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged) return MPSP_E_ARG;
+  if (at.device != dev) return MPSP_E_DEVICE;
+  return MPSP_OK;
+}
+
+__attribute__((unused)) int validate_x_host(int L, int64_t n, const uint32_t* xl, const int32_t* xe) {
+  for (int64_t i = 0; i < n; ++i) {
+    const uint32_t top = xl[(size_t)i * L + L - 1];
+    bool nz = false;
+    for (int c = 0; c < L; ++c) nz |= xl[(size_t)i * L + c] != 0u;
+    if (nz && !(top >> 31)) return MPSP_E_VALUE;
+    if (nz && (xe[i] > (1 << 29) || xe[i] < -(1 << 29))) return MPSP_E_VALUE;
+  }
+  return MPSP_OK;
+}
+
+int do_spmv(const mpsp_csr* A, bool transpose, const uint32_t* xl, const int32_t* xe,
+            const uint8_t* xs, uint32_t* yl, int32_t* ye, uint8_t* ys, void* stream,
+            bool check_ptrs) {
+  if (!A) return MPSP_E_ARG;
+  if (transpose && !A->has_t) return MPSP_E_NOTRANS;
+  const int L = A->L;
+  // empty x / y may be passed as NULL
+  if ((A->n > 0 && (!xl || !xe || !xs)) || (A->re > A->rb && (!yl || !ye || !ys))) return MPSP_E_ARG;
+  if (A->n == 0 && A->re == A->rb) return MPSP_OK;
+  const size_t align = (size_t)(L >= 4 ? 16 : 4 * L);
+  if (((uintptr_t)xl % align) || ((uintptr_t)yl % align)) return MPSP_E_ARG;
+  const int64_t n = A->n, r = A->re - A->rb;
+  const size_t xb[3] = {(size_t)n * L * 4, (size_t)n * 4, (size_t)n};
+  const size_t yb[3] = {(size_t)r * L * 4, (size_t)r * 4, (size_t)r};
+  const void* xp[3] = {xl, xe, xs};
+  const void* yp[3] = {yl, ye, ys};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      if (overlap(xp[i], xb[i], yp[j], yb[j])) return MPSP_E_ALIAS;
+  int cur = -1;
+  cudaError_t e = cudaGetDevice(&cur);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (cur != A->dev) return MPSP_E_DEVICE;
+  if (check_ptrs) {
+    for (int i = 0; i < 3; ++i) {
+      int rc = n > 0 ? check_device_ptr(xp[i], A->dev) : MPSP_OK;
+      if (rc) return rc;
+      rc = r > 0 ? check_device_ptr(yp[i], A->dev) : MPSP_OK;
+      if (rc) return rc;
+    }
+  }
+  if (env_validate() && n > 0) {
+    std::vector<uint32_t> hl((size_t)n * L);
+    std::vector<int32_t> he((size_t)n);
+    if (cudaMemcpy(hl.data(), xl, hl.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(he.data(), xe, he.size() * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return cuda_fail(cudaGetLastError());
+    int rc = validate_x_host(L, n, hl.data(), he.data());
+    if (rc) return rc;
+  }
+  if (r == 0) return MPSP_OK;
+  const DevPart& P = transpose ? A->T : A->A;
+  XView xv{xl, xe, xs};
+  YView yv{yl, ye, ys};
+  int err = launch_spmv(L, P.view(), xv, yv, stream);
+  if (err != 0) return cuda_fail((cudaError_t)err);
+  return MPSP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mpsp_strerror(int code) {
+  switch (code) {
+    case MPSP_OK: return "ok";
+    case MPSP_E_ARG: return "invalid argument (null pointer, bad size or range, misaligned)";
+    case MPSP_E_PREC: return "unsupported precision (p must be 32, 64, 128, 256, 512 or 1024)";
+    case MPSP_E_CSR: return "invalid CSR structure (rowptr/colidx)";
+    case MPSP_E_UNSORTED: return "column indices not strictly increasing within a row";
+    case MPSP_E_VALUE: return "invalid value (unnormalised nonzero mantissa or |exp| > 2^29)";
+    case MPSP_E_NOMEM: return "out of memory";
+    case MPSP_E_CUDA: return "CUDA error";
+    case MPSP_E_ALIAS: return "x and y storage overlap";
+    case MPSP_E_DEVICE: return "wrong CUDA device for this handle";
+    case MPSP_E_NOTRANS: return "handle built without MPSP_WITH_TRANSPOSE";
+    default: return "unknown error code";
+  }
+}
+
+const char* mpsp_last_cuda_error(void) { return g_cuda_err; }
+
+int mpsp_supported_precision(int p_bits) { return p_bits > 0 && p_bits % 32 == 0 && supported_L(p_bits / 32); }
+
+int64_t mpsp_launch_count(void) { return launch_counter_get(); }
+
+int mpsp_csr_create(mpsp_csr** out, int p_bits, int64_t n, const int64_t* rowptr,
+                    const int32_t* colidx, const uint32_t* limbs, const int32_t* exps,
+                    const uint8_t* signs, int64_t row_begin, int64_t row_end, uint32_t flags) {
+  if (!out) return MPSP_E_ARG;
+  *out = nullptr;
+  if (n < 0 || !rowptr || row_begin < 0 || row_end < row_begin || row_end > n) return MPSP_E_ARG;
+  if (flags & ~MPSP_WITH_TRANSPOSE) return MPSP_E_ARG;
+  if (!mpsp_supported_precision(p_bits)) return MPSP_E_PREC;
+  if (n > INT32_MAX) return MPSP_E_CSR;
+  const int L = p_bits / 32;
+  // ---- a1: CSR invariants
+  if (rowptr[0] != 0) return MPSP_E_CSR;
+  for (int64_t i = 0; i < n; ++i)
+    if (rowptr[i + 1] < rowptr[i]) return MPSP_E_CSR;
+  const int64_t nnz = rowptr[n];
+  if (nnz > INT32_MAX) return MPSP_E_CSR;
+  if (nnz > 0 && (!colidx || !limbs || !exps || !signs)) return MPSP_E_ARG;
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+      if (colidx[k] < 0 || colidx[k] >= n) return MPSP_E_CSR;
+    }
+  }
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t k = rowptr[i] + 1; k < rowptr[i + 1]; ++k)
+      if (colidx[k] <= colidx[k - 1]) return MPSP_E_UNSORTED;
+  // ---- value encodings
+  {
+    std::atomic<int> bad{0};
+    parallel_for(nnz, [&](int64_t k0, int64_t k1) {
+      for (int64_t k = k0; k < k1; ++k) {
+        const uint32_t* m = limbs + (size_t)k * L;
+        bool nz = false;
+        for (int c = 0; c < L; ++c) nz |= m[c] != 0u;
+        if (!nz) continue;
+        if (!(m[L - 1] >> 31) || exps[k] > (1 << 29) || exps[k] < -(1 << 29)) bad.store(1);
+      }
+    });
+    if (bad.load()) return MPSP_E_VALUE;
+  }
+  int dev = 0;
+  cudaError_t ce = cudaGetDevice(&dev);
+  if (ce != cudaSuccess) return cuda_fail(ce);
+  mpsp_csr* H = new (std::nothrow) mpsp_csr();
+  if (!H) return MPSP_E_NOMEM;
+  H->dev = dev; H->p = p_bits; H->L = L; H->n = n; H->rb = row_begin; H->re = row_end;
+  H->flags = flags;
+  const int64_t nrows = row_end - row_begin;
+  int rc = MPSP_OK;
+  // ---- part A: rows [rb, re)
+  {
+    std::vector<int64_t> lrp((size_t)nrows + 1);
+    const int64_t k0 = rowptr[row_begin];
+    for (int64_t r = 0; r <= nrows; ++r) lrp[(size_t)r] = rowptr[row_begin + r] - k0;
+    rc = build_part(H->A, L, nrows, lrp.data(), colidx + k0, nullptr, k0, limbs, exps, signs);
+  }
+  // ---- a2: transpose (stable counting sort on column), rows [rb, re) of A^T
+  if (rc == MPSP_OK && (flags & MPSP_WITH_TRANSPOSE)) {
+    H->has_t = true;
+    try {
+      std::vector<int64_t> tcnt((size_t)n + 1, 0);
+      for (int64_t k = 0; k < nnz; ++k) tcnt[(size_t)colidx[k] + 1]++;
+      for (int64_t j = 0; j < n; ++j) tcnt[(size_t)j + 1] += tcnt[(size_t)j];
+      const int64_t t0 = tcnt[(size_t)row_begin], t1 = tcnt[(size_t)row_end];
+      std::vector<int64_t> next(tcnt.begin(), tcnt.end() - 1);
+      std::vector<int32_t> tcol((size_t)(t1 - t0));
+      std::vector<int64_t> tsrc((size_t)(t1 - t0));
+      for (int64_t i = 0; i < n; ++i) {          // ascending row index of A
+        for (int64_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+          const int64_t j = colidx[k];
+          if (j < row_begin || j >= row_end) continue;
+          const int64_t pos = next[(size_t)j]++ - t0;
+          tcol[(size_t)pos] = (int32_t)i;
+          tsrc[(size_t)pos] = k;
+        }
+      }
+      std::vector<int64_t> lrp((size_t)nrows + 1);
+      for (int64_t r = 0; r <= nrows; ++r) lrp[(size_t)r] = tcnt[(size_t)(row_begin + r)] - t0;
+      rc = build_part(H->T, L, nrows, lrp.data(), tcol.data(), tsrc.data(), 0, limbs, exps, signs);
+    } catch (const std::bad_alloc&) {
+      rc = MPSP_E_NOMEM;
+    }
+  }
+  if (rc == MPSP_OK) {
+    ce = cudaDeviceSynchronize();
+    if (ce != cudaSuccess) rc = cuda_fail(ce);
+  }
+  if (rc != MPSP_OK) {
+    mpsp_destroy(H);
+    return rc;
+  }
+  *out = H;
+  return MPSP_OK;
+}
+
+void mpsp_destroy(mpsp_csr* A) {
+  if (!A) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(A->dev);
+  cudaDeviceSynchronize();
+  A->A.release();
+  A->T.release();
+  if (A->ws) cudaFree(A->ws);
+  if (A->stream) cudaStreamDestroy(A->stream);
+  cudaSetDevice(cur);
+  cudaGetLastError();
+  delete A;
+}
+
+int mpsp_spmv(const mpsp_csr* A, const uint32_t* x_limbs, const int32_t* x_exps,
+              const uint8_t* x_signs, uint32_t* y_limbs, int32_t* y_exps, uint8_t* y_signs,
+              void* cuda_stream) {
+  return do_spmv(A, false, x_limbs, x_exps, x_signs, y_limbs, y_exps, y_signs, cuda_stream, true);
+}
+
+int mpsp_spmv_t(const mpsp_csr* A, const uint32_t* x_limbs, const int32_t* x_exps,
+                const uint8_t* x_signs, uint32_t* y_limbs, int32_t* y_exps, uint8_t* y_signs,
+                void* cuda_stream) {
+  return do_spmv(A, true, x_limbs, x_exps, x_signs, y_limbs, y_exps, y_signs, cuda_stream, true);
+}
+
+static int spmv_host(mpsp_csr* A, bool transpose, const uint32_t* xl, const int32_t* xe,
+                     const uint8_t* xs, uint32_t* yl, int32_t* ye, uint8_t* ys) {
+  if (!A) return MPSP_E_ARG;
+  if (transpose && !A->has_t) return MPSP_E_NOTRANS;
+  const int L = A->L;
+  const int64_t n = A->n, r = A->re - A->rb;
+  if ((n > 0 && (!xl || !xe || !xs)) || (r > 0 && (!yl || !ye || !ys))) return MPSP_E_ARG;
+  if (n == 0 && r == 0) return MPSP_OK;
+  const size_t xb[3] = {(size_t)n * L * 4, (size_t)n * 4, (size_t)n};
+  const size_t yb[3] = {(size_t)r * L * 4, (size_t)r * 4, (size_t)r};
+  const void* xp[3] = {xl, xe, xs};
+  const void* yp[3] = {yl, ye, ys};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      if (overlap(xp[i], xb[i], yp[j], yb[j])) return MPSP_E_ALIAS;
+  int cur = -1;
+  cudaError_t e = cudaGetDevice(&cur);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (cur != A->dev) return MPSP_E_DEVICE;
+  auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  const size_t need = al(xb[0]) + al(xb[1]) + al(xb[2]) + al(yb[0]) + al(yb[1]) + al(yb[2]) + 256;
+  if (!A->stream) {
+    e = cudaStreamCreateWithFlags(&A->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  if (A->ws_bytes < need) {
+    if (A->ws) cudaFree(A->ws);
+    A->ws = nullptr;
+    A->ws_bytes = 0;
+    e = cudaMalloc(&A->ws, need);
+    if (e != cudaSuccess) { cudaGetLastError(); return MPSP_E_NOMEM; }
+    A->ws_bytes = need;
+  }
+  char* base = (char*)A->ws;
+  void* dx[3];
+  void* dy[3];
+  size_t off = 0;
+  for (int i = 0; i < 3; ++i) { dx[i] = base + off; off += al(xb[i]); }
+  for (int i = 0; i < 3; ++i) { dy[i] = base + off; off += al(yb[i]); }
+  for (int i = 0; i < 3; ++i)
+    if (xb[i] && (e = cudaMemcpyAsync(dx[i], xp[i], xb[i], cudaMemcpyHostToDevice, A->stream)) != cudaSuccess)
+      return cuda_fail(e);
+  int rc = do_spmv(A, transpose, (const uint32_t*)dx[0], (const int32_t*)dx[1], (const uint8_t*)dx[2],
+                   (uint32_t*)dy[0], (int32_t*)dy[1], (uint8_t*)dy[2], A->stream, false);
+  if (rc) return rc;
+  void* hy[3] = {yl, ye, ys};
+  for (int i = 0; i < 3; ++i)
+    if (yb[i] && (e = cudaMemcpyAsync(hy[i], dy[i], yb[i], cudaMemcpyDeviceToHost, A->stream)) != cudaSuccess)
+      return cuda_fail(e);
+  e = cudaStreamSynchronize(A->stream);
+  if (e != cudaSuccess) return cuda_fail(e);
+  return MPSP_OK;
+}
+
+int mpsp_spmv_host(mpsp_csr* A, const uint32_t* x_limbs, const int32_t* x_exps,
+                   const uint8_t* x_signs, uint32_t* y_limbs, int32_t* y_exps, uint8_t* y_signs) {
+  return spmv_host(A, false, x_limbs, x_exps, x_signs, y_limbs, y_exps, y_signs);
+}
+
+int mpsp_spmv_t_host(mpsp_csr* A, const uint32_t* x_limbs, const int32_t* x_exps,
+                     const uint8_t* x_signs, uint32_t* y_limbs, int32_t* y_exps, uint8_t* y_signs) {
+  return spmv_host(A, true, x_limbs, x_exps, x_signs, y_limbs, y_exps, y_signs);
+}
+
+int mpsp_csr_info(const mpsp_csr* A, int64_t info[10]) {
+  if (!A || !info) return MPSP_E_ARG;
+  info[0] = A->p;
+  info[1] = A->n;
+  info[2] = A->rb;
+  info[3] = A->re;
+  info[4] = A->A.nnz;
+  info[5] = A->has_t ? A->T.nnz : -1;
+  info[6] = (int64_t)(A->A.bytes + A->T.bytes + A->ws_bytes);
+  info[7] = A->dev;
+  info[8] = A->A.nentries;
+  info[9] = A->A.max_len;
+  return MPSP_OK;
+}
+
+int mpsp_imad_bench(double out[3]) {
+  if (!out) return MPSP_E_ARG;
+  int e = run_imad_bench(out);
+  if (e != 0) return cuda_fail((cudaError_t)e);
+  return MPSP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,190 @@
+"""GPU tests of the C ABI contract and of invariants the CUDA path must obey
+(SURVEY.md 4 T2/T4/T5'): error codes, ownership, host-buffer entry points,
+row-range handles, determinism, identity/permutation/scaling/negation and
+explicit zeros - all bit-exact."""
+import ctypes
+
+import numpy as np
+import pytest
+
+import gen
+from gpu_util import assert_same, gpu_run, oracle_full
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    import __graft_entry__
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    __graft_entry__.build()
+
+
+def _csr(d, **kw):
+    from paper_1411_2377_b200 import CSR
+    return CSR(d["p"], d["rowptr"], d["colidx"], d["limbs"], d["exps"], d["signs"], **kw)
+
+
+def _x(d):
+    from paper_1411_2377_b200 import MPVec
+    return MPVec.from_host(d["x_limbs"], d["x_exps"], d["x_signs"], device="cuda:0")
+
+
+def test_notrans_alias_misaligned():
+    import torch
+    from paper_1411_2377_b200 import MPVec, MpspError
+    from paper_1411_2377_b200 import _lib
+    d = gen.make("C1", n=200)
+    A = _csr(d)
+    x = _x(d)
+    with pytest.raises(MpspError) as e:
+        A.spmv_t(x)
+    assert e.value.name == "MPSP_E_NOTRANS"
+    # aliasing: y's limbs on top of x's limbs
+    y = MPVec(x.limbs, torch.empty_like(x.exps), torch.empty_like(x.signs))
+    with pytest.raises(MpspError) as e:
+        A.spmv(x, out=y)
+    assert e.value.name == "MPSP_E_ALIAS"
+    # misaligned limbs pointer
+    buf = torch.zeros(d["n"] * 4 + 1, dtype=torch.int32, device="cuda:0")
+    y = MPVec.empty(d["n"], 4)
+    rc = _lib.lib().mpsp_spmv(A._h, buf.data_ptr() + 4, x.exps.data_ptr(), x.signs.data_ptr(),
+                              y.limbs.data_ptr(), y.exps.data_ptr(), y.signs.data_ptr(), None)
+    assert rc == _lib.ERROR_CODES["MPSP_E_ARG"]
+    # host pointer passed to the device entry point
+    hx = np.zeros((d["n"], 4), np.uint32)
+    rc = _lib.lib().mpsp_spmv(A._h, hx.ctypes.data, x.exps.data_ptr(), x.signs.data_ptr(),
+                              y.limbs.data_ptr(), y.exps.data_ptr(), y.signs.data_ptr(), None)
+    assert rc == _lib.ERROR_CODES["MPSP_E_ARG"]
+    A.close()
+
+
+def test_handle_owns_copies_and_host_entry_points():
+    d = gen.make("C1", n=500, seed=5)
+    want = oracle_full(d, "ax")
+    want_t = oracle_full(d, "atx")
+    keep = {k: d[k].copy() for k in ("limbs", "exps", "signs", "colidx")}
+    A = _csr(d, transpose=True)
+    d["limbs"][:] = 0xFFFFFFFF                    # mutate inputs after create
+    d["exps"][:] = 7
+    x = _x(d)
+    assert_same(A.spmv(x).to_host(), want, "after mutating host inputs")
+    assert_same(A.spmv_host(d["x_limbs"], d["x_exps"], d["x_signs"]), want, "spmv_host")
+    assert_same(A.spmv_t_host(d["x_limbs"], d["x_exps"], d["x_signs"]), want_t, "spmv_t_host")
+    info = A.info()
+    assert info["nnz"] == len(keep["colidx"]) and info["nnz_t"] == len(keep["colidx"])
+    assert info["max_row"] == 8
+    A.close()
+    A.close()                                     # idempotent
+
+
+@pytest.mark.parametrize("op", ["ax", "atx"])
+def test_row_range_handles_concatenate(op):
+    """T5': G row-range handles over the full x == the full result (no NCCL)."""
+    d = gen.make("C4", n=6000, seed=7)
+    full = gpu_run(d, op)
+    n = d["n"]
+    for G in (2, 3, 8):
+        blk = (n + G - 1) // G
+        parts = [gpu_run(d, op, rows=(min(r * blk, n), min((r + 1) * blk, n))) for r in range(G)]
+        cat = tuple(np.concatenate([p_[i] for p_ in parts]) for i in range(3))
+        assert_same(cat, full, f"G={G} {op}")
+
+
+def test_determinism_repeated_application():
+    d = gen.make("C3", n=8000, seed=9)
+    A = _csr(d)
+    x = _x(d)
+    r0 = A.spmv(x).to_host()
+    for _ in range(5):
+        assert_same(A.spmv(x).to_host(), r0, "repeat")
+    A.close()
+
+
+def test_identity_permutation_scaling_negation():
+    p = 256
+    L = p // 32
+    n = 3000
+    d = gen.make("C3", n=n, p=p, seed=11)
+    one = np.zeros((n, L), np.uint32)
+    one[:, -1] = 0x80000000
+    # identity
+    ident = dict(p=p, n=n, rowptr=np.arange(n + 1, dtype=np.int64),
+                 colidx=np.arange(n, dtype=np.int32), limbs=one, exps=np.ones(n, np.int32),
+                 signs=np.zeros(n, np.uint8), x_limbs=d["x_limbs"], x_exps=d["x_exps"],
+                 x_signs=d["x_signs"])
+    y = gpu_run(ident, "ax")
+    assert_same(y, (d["x_limbs"], d["x_exps"], d["x_signs"]), "identity")
+    # permutation
+    perm = np.random.default_rng(1).permutation(n).astype(np.int32)
+    P = dict(ident, colidx=perm)
+    assert_same(gpu_run(P, "ax"), (d["x_limbs"][perm], d["x_exps"][perm], d["x_signs"][perm]), "perm")
+    # 2^k scaling and negation of A
+    base = gpu_run(d, "ax")
+    nz = np.any(base[0] != 0, axis=1)
+    for k in (-7, 3):
+        ds = dict(d, exps=d["exps"] + k)
+        want = (base[0], np.where(nz, base[1] + k, 0).astype(np.int32), base[2])
+        assert_same(gpu_run(ds, "ax"), want, f"2^{k} scaling")
+    dn = dict(d, signs=(1 - d["signs"]).astype(np.uint8))
+    want = (base[0], base[1], np.where(nz, 1 - base[2], 0).astype(np.uint8))
+    assert_same(gpu_run(dn, "ax"), want, "negation")
+
+
+def test_explicit_zeros_change_nothing():
+    """Insert explicit zero entries (junk sign/exp) into every row."""
+    d = gen.make("C1", n=400, seed=12)
+    base = gpu_run(d, "ax")
+    n, L = d["n"], d["p"] // 32
+    rp, ci = d["rowptr"], d["colidx"]
+    rows, cols, li, ex, sg = [], [], [], [], []
+    rng = np.random.default_rng(3)
+    for i in range(n):
+        existing = set(ci[rp[i]:rp[i + 1]].tolist())
+        extra = [c for c in rng.choice(n, 6, replace=False).tolist() if c not in existing][:3]
+        ent = [(c, d["limbs"][k], d["exps"][k], d["signs"][k]) for k, c in
+               zip(range(rp[i], rp[i + 1]), ci[rp[i]:rp[i + 1]])]
+        ent += [(c, np.zeros(L, np.uint32), rng.integers(-99, 99), rng.integers(0, 2)) for c in extra]
+        ent.sort(key=lambda t: t[0])
+        for c, l_, e_, s_ in ent:
+            rows.append(i); cols.append(c); li.append(l_); ex.append(e_); sg.append(s_)
+    rowptr = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=rowptr[1:])
+    dz = dict(d, rowptr=rowptr, colidx=np.array(cols, np.int32), limbs=np.array(li, np.uint32),
+              exps=np.array(ex, np.int32), signs=np.array(sg, np.uint8))
+    assert_same(gpu_run(dz, "ax"), base, "explicit zeros")
+
+
+def test_empty_matrix_and_empty_rows():
+    from paper_1411_2377_b200 import CSR, MPVec
+    p, L, n = 128, 4, 70
+    rowptr = np.zeros(n + 1, np.int64)
+    A = CSR(p, rowptr, np.zeros(0, np.int32), np.zeros((0, L), np.uint32), np.zeros(0, np.int32),
+            np.zeros(0, np.uint8), transpose=True)
+    xl = np.zeros((n, L), np.uint32)
+    xl[:, -1] = 0x80000000
+    x = MPVec.from_host(xl, np.ones(n, np.int32), np.ones(n, np.uint8))
+    for y in (A.spmv(x), A.spmv_t(x)):
+        yl, ye, ys = y.to_host()
+        assert not yl.any() and not ye.any() and not ys.any()
+    A.close()
+    # n = 0
+    A = CSR(p, np.zeros(1, np.int64), np.zeros(0, np.int32), np.zeros((0, L), np.uint32),
+            np.zeros(0, np.int32), np.zeros(0, np.uint8))
+    y = A.spmv(MPVec.empty(0, L))
+    assert y.n == 0
+    A.close()
+
+
+def test_launch_counter_counts_kernels():
+    from paper_1411_2377_b200 import launch_count
+    d = gen.make("C1", n=100)
+    A = _csr(d)
+    x = _x(d)
+    c0 = launch_count()
+    for _ in range(3):
+        A.spmv(x)
+    assert launch_count() - c0 >= 3
+    A.close()

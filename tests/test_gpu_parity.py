@@ -1,0 +1,81 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit-exact
+(every limb, exponent and sign; integer/byte work -> bit-exact bar).
+
+Cases: the stress corpus (every rounding corner, rows of length 0..5000) at
+every supported p, the hand-worked golden examples, and C1-C5 recipes at
+oracle-sized n spanning many slices with ragged tails, for A x and A^T x.
+Full-size configs are checked on sampled rows in test_gpu_fullsize.py.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import gen
+from gpu_util import assert_same, gpu_run, oracle_full
+
+pytestmark = pytest.mark.gpu
+
+PS = [32, 64, 128, 256, 512, 1024]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    import __graft_entry__
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    __graft_entry__.build()
+
+
+@pytest.mark.parametrize("op", ["ax", "atx"])
+@pytest.mark.parametrize("p", PS)
+def test_stress_corpus(p, op):
+    d = gen.stress(p, seed=0)
+    assert_same(gpu_run(d, op), oracle_full(d, op), f"stress p={p} {op}")
+
+
+@pytest.mark.parametrize("p", [64, 256, 1024])
+def test_stress_corpus_other_seed(p):
+    d = gen.stress(p, seed=1, long_len=2000)
+    for op in ("ax", "atx"):
+        assert_same(gpu_run(d, op), oracle_full(d, op), f"stress seed1 p={p} {op}")
+
+
+def test_golden_examples_on_gpu():
+    from test_oracle_pins import GOLDEN, T
+    g = json.load(open(GOLDEN))
+    for c in g["spmv"]:
+        p = c["p"]
+        A = [T(v, p) for v in c["A"]]
+        x = [T(v, p) for v in c["x"]]
+        al, ae, as_ = gen.pack_triples(A, p)
+        xl, xe, xs = gen.pack_triples(x, p)
+        d = dict(p=p, n=c["n"], rowptr=np.array(c["rowptr"], np.int64),
+                 colidx=np.array(c["colidx"], np.int32), limbs=al, exps=ae, signs=as_,
+                 x_limbs=xl, x_exps=xe, x_signs=xs)
+        want = gen.pack_triples([T(v, p) for v in c["y"]], p)
+        assert_same(gpu_run(d, "ax"), want, c["name"])
+        if "yt" in c:
+            want = gen.pack_triples([T(v, p) for v in c["yt"]], p)
+            assert_same(gpu_run(d, "atx"), want, c["name"] + " (A^T)")
+
+
+CFG_SMALL = [("C1", None), ("C2", 20_000), ("C3", 20_000), ("C4", 20_000), ("C5", 10_000)]
+
+
+@pytest.mark.parametrize("cfg,n", CFG_SMALL)
+def test_config_recipes_small(cfg, n):
+    d = gen.make(cfg, n=n, seed=2)
+    ops = ["ax", "atx"]
+    for op in ops:
+        assert_same(gpu_run(d, op), oracle_full(d, op), f"{cfg} n={d['n']} {op}")
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C3", "C5"])
+@pytest.mark.parametrize("p", [32, 64, 512])
+def test_config_recipes_other_precisions(cfg, p):
+    n = {"C1": 1000, "C3": 3000, "C5": 2500}[cfg]
+    d = gen.make(cfg, n=n, p=p, seed=3)
+    assert_same(gpu_run(d, "ax"), oracle_full(d, "ax"), f"{cfg} p={p}")
