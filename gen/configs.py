@@ -243,7 +243,7 @@ def stencil_values(rng, is_diag, L):
     signs = np.ones(nnz, dtype=np.uint8)
     # a k>0 low field of all zeros would be M = 2^p - 0: not representable
     low_zero = pos & np.all(limbs[:, :] == np.where(np.arange(L) == L - 1, top20, 0), axis=1)
-    limbs[low_zero, 0] = 2
+    limbs[low_zero, 0] |= np.uint32(2)
     limbs[is_diag] = 0
     limbs[is_diag, L - 1] = np.uint32(0x80000000)
     exps[is_diag] = 3
