@@ -27,6 +27,57 @@ __device__ __forceinline__ void mac3(uint32_t& c0, uint32_t& c1, uint32_t& c2,
       : "r"(a), "r"(b));
 }
 
+// --------------------------------------------------------------------------
+// Carry-chain helpers (PTX add.cc/addc/sub.cc/subc: one instruction per limb;
+// the chains are emitted in order by consecutive asm volatile statements).
+// --------------------------------------------------------------------------
+// z = x + y (N limbs); returns the carry out (0/1)
+template <int N>
+__device__ __forceinline__ uint32_t add_n(uint32_t (&z)[N], const uint32_t (&x)[N],
+                                          const uint32_t (&y)[N]) {
+  uint32_t c;
+  asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(z[0]) : "r"(x[0]), "r"(y[0]));
+#pragma unroll
+  for (int i = 1; i < N; ++i)
+    asm volatile("addc.cc.u32 %0, %1, %2;" : "=r"(z[i]) : "r"(x[i]), "r"(y[i]));
+  asm volatile("addc.u32 %0, 0, 0;" : "=r"(c));
+  return c;
+}
+// z = x - y - b0 (N limbs, b0 in {0,1}); returns the borrow out (0/1)
+template <int N>
+__device__ __forceinline__ uint32_t sub_n(uint32_t (&z)[N], const uint32_t (&x)[N],
+                                          const uint32_t (&y)[N], uint32_t b0) {
+  uint32_t b, dummy;
+  // set the carry flag to b0 via 0 - b0 (borrow iff b0 = 1)
+  asm volatile("sub.cc.u32 %0, 0, %1;" : "=r"(dummy) : "r"(b0));
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+    asm volatile("subc.cc.u32 %0, %1, %2;" : "=r"(z[i]) : "r"(x[i]), "r"(y[i]));
+  asm volatile("subc.u32 %0, 0, 0;" : "=r"(b));
+  return b & 1u;
+}
+// borrow of x - y (N limbs) without storing the difference: 1 iff x < y
+template <int N>
+__device__ __forceinline__ uint32_t lt_n(const uint32_t (&x)[N], const uint32_t (&y)[N]) {
+  uint32_t b, d;
+  asm volatile("sub.cc.u32 %0, %1, %2;" : "=r"(d) : "r"(x[0]), "r"(y[0]));
+#pragma unroll
+  for (int i = 1; i < N; ++i)
+    asm volatile("subc.cc.u32 %0, %1, %2;" : "=r"(d) : "r"(x[i]), "r"(y[i]));
+  asm volatile("subc.u32 %0, 0, 0;" : "=r"(b));
+  return b & 1u;
+}
+// m += inc (inc in {0,1}); returns the carry out of the top limb
+template <int N>
+__device__ __forceinline__ uint32_t inc_n(uint32_t (&m)[N], uint32_t inc) {
+  uint32_t c;
+  asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(m[0]) : "r"(inc));
+#pragma unroll
+  for (int i = 1; i < N; ++i) asm volatile("addc.cc.u32 %0, %0, 0;" : "+r"(m[i]));
+  asm volatile("addc.u32 %0, 0, 0;" : "=r"(c));
+  return c;
+}
+
 // Register-resident MP number.  m[L-1] == 0 <=> zero.
 template <int L>
 struct MP {
@@ -47,14 +98,8 @@ struct MP {
 // caller renormalises to 2^(p-1) and bumps the exponent).
 template <int L>
 __device__ __forceinline__ uint32_t rne_increment(uint32_t (&m)[L], uint32_t rb, uint32_t sticky) {
-  uint32_t c = rb & ((sticky != 0u) | (m[0] & 1u));
-#pragma unroll
-  for (int i = 0; i < L; ++i) {
-    uint64_t t = (uint64_t)m[i] + c;
-    m[i] = (uint32_t)t;
-    c = (uint32_t)(t >> 32);
-  }
-  return c;
+  const uint32_t inc = rb & ((sticky != 0u) | (m[0] & 1u));
+  return inc_n<L>(m, inc);
 }
 
 // --------------------------------------------------------------------------
@@ -83,23 +128,17 @@ __device__ __forceinline__ void mp_mul(const uint32_t (&a)[L], int32_t ea, uint3
     c0 = c1; c1 = c2; c2 = 0u;
   }
   P[L - 1] = c0;                           // limb 2L-1
-  const bool top = (P[L - 1] >> 31) != 0u;
-  uint32_t rb, st;
-  if (top) {
+  // normalise: shift left by sh = 1 when the top product bit is clear
+  const uint32_t sh = (~P[L - 1]) >> 31;
 #pragma unroll
-    for (int i = 0; i < L; ++i) t.m[i] = P[i];
-    rb = w >> 31;
-    st = sticky | (w << 1);
-  } else {
-#pragma unroll
-    for (int i = L - 1; i > 0; --i) t.m[i] = __funnelshift_l(P[i - 1], P[i], 1);
-    t.m[0] = __funnelshift_l(w, P[0], 1);
-    rb = (w >> 30) & 1u;
-    st = sticky | (w << 2);
-  }
+  for (int i = L - 1; i > 0; --i) t.m[i] = __funnelshift_l(P[i - 1], P[i], sh);
+  t.m[0] = __funnelshift_l(w, P[0], sh);
+  const uint32_t ws = w << sh;             // w's bits below the new LSB
+  const uint32_t rb = ws >> 31;
+  const uint32_t st = sticky | (ws << 1);
   const uint32_t cy = rne_increment<L>(t.m, rb, st);
   if (cy) t.m[L - 1] = 0x80000000u;
-  t.e = ea + ex - (top ? 0 : 1) + (int32_t)cy;
+  t.e = ea + ex - (int32_t)sh + (int32_t)cy;
   t.s = sa ^ sx;
 }
 
@@ -110,15 +149,20 @@ __device__ __forceinline__ void mp_mul(const uint32_t (&a)[L], int32_t ea, uint3
 template <int N>
 __device__ __forceinline__ void shr_bits_sticky(uint32_t (&v)[N], uint32_t d, uint32_t& sticky) {
   const uint32_t q = d >> 5, r = d & 31u;
+  // limb steps only up to the largest limb shift any active lane needs
+  // (warp-uniform branch: no divergence, no dynamic register indexing)
+  const uint32_t qmax = __reduce_max_sync(__activemask(), q);
 #pragma unroll
-  for (int b = 1; b < N; b <<= 1) {
-    const bool on = (q & (uint32_t)b) != 0u;
-    uint32_t drop = 0u;
+  for (int b = 1; b <= N; b <<= 1) {
+    if (qmax >= (uint32_t)b) {
+      const bool on = (q & (uint32_t)b) != 0u;
+      uint32_t drop = 0u;
 #pragma unroll
-    for (int i = 0; i < b; ++i) drop |= v[i];
-    sticky |= on ? drop : 0u;
+      for (int i = 0; i < b; ++i) drop |= v[i];
+      sticky |= on ? drop : 0u;
 #pragma unroll
-    for (int i = 0; i < N; ++i) v[i] = on ? (i + b < N ? v[i + b] : 0u) : v[i];
+      for (int i = 0; i < N; ++i) v[i] = on ? (i + b < N ? v[i + b] : 0u) : v[i];
+    }
   }
   sticky |= r ? (v[0] << (32u - r)) : 0u;
 #pragma unroll
@@ -162,74 +206,65 @@ __device__ __forceinline__ uint32_t clz_limbs(const uint32_t (&v)[N]) {
 // --------------------------------------------------------------------------
 template <int L>
 __device__ __forceinline__ void mp_add(MP<L>& s, const MP<L>& t) {
-  if (t.is_zero()) return;
-  if (s.is_zero()) { s = t; return; }
-  // |t| > |s| ?  compare (e, M)
-  uint32_t borrow = 0u;
-#pragma unroll
-  for (int i = 0; i < L; ++i) {
-    uint64_t dd = (uint64_t)s.m[i] - t.m[i] - borrow;
-    borrow = (uint32_t)(dd >> 63);
-  }
-  const bool t_big = (t.e > s.e) || (t.e == s.e && borrow);
-  uint32_t X[L + 1], Y[L + 1];
-  X[0] = 0u;
-  Y[0] = 0u;
-#pragma unroll
-  for (int i = 0; i < L; ++i) {
-    X[i + 1] = t_big ? t.m[i] : s.m[i];
-    Y[i + 1] = t_big ? s.m[i] : t.m[i];
-  }
+  // Branch-free zero handling: a zero operand becomes the "small" operand
+  // with d = 0 and contributes nothing; both zero gives a zero mantissa.
+  const bool tz = t.is_zero(), sz = s.is_zero();
+  const uint32_t mlt = lt_n<L>(s.m, t.m);               // |M_s| < |M_t|
+  const bool t_big = !tz && (sz || t.e > s.e || (t.e == s.e && mlt));
   const int32_t eb = t_big ? t.e : s.e;
   const int32_t esm = t_big ? s.e : t.e;
   const uint32_t sb = t_big ? t.s : s.s;
   const bool same = (t.s == s.s);
-  const uint32_t d = (uint32_t)eb - (uint32_t)esm;      // exact as uint32
-  if (d >= (uint32_t)(32 * L + 2)) {                    // far-path lemma
-    if (t_big) s = t;
-    return;
+  uint32_t d = (uint32_t)eb - (uint32_t)esm;            // exact as uint32
+  d = (tz || sz) ? 0u : min(d, (uint32_t)(32 * (L + 1)));  // d >= p+2: all sticky
+  // Z = big * 2^32 (guard limb Z[0]); Y = small * 2^32, to be aligned
+  uint32_t Z[L + 1], Y[L + 1];
+  Z[0] = 0u;
+  Y[0] = 0u;
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    Z[i + 1] = t_big ? t.m[i] : s.m[i];
+    Y[i + 1] = t_big ? s.m[i] : t.m[i];
   }
-  uint32_t stk = 0u;
-  shr_bits_sticky<L + 1>(Y, d, stk);
-  uint32_t Z[L + 1];
   int32_t e;
-  uint32_t rb, st;
-  if (same) {
-    uint32_t c = 0u;
+  uint32_t stk = 0u;
+  if (!same && d <= 1u) {
+    // ---- near path: exact subtraction, then normalise left by lz
 #pragma unroll
-    for (int i = 0; i <= L; ++i) {
-      uint64_t tt = (uint64_t)X[i] + Y[i] + c;
-      Z[i] = (uint32_t)tt;
-      c = (uint32_t)(tt >> 32);
+    for (int i = 0; i < L; ++i) Y[i] = __funnelshift_r(Y[i], Y[i + 1], d);
+    Y[L] >>= d;
+    sub_n<L + 1>(Z, Z, Y, 0u);
+    uint32_t lz = __clz(Z[L]);
+    if (lz < 32u) {
+#pragma unroll
+      for (int i = L; i > 0; --i) Z[i] = __funnelshift_l(Z[i - 1], Z[i], lz);
+      Z[0] <<= lz;
+    } else {            // >= 32 bits cancelled, or exact zero (rare)
+      lz = clz_limbs<L + 1>(Z);
+      shl_bits<L + 1>(Z, lz);
     }
-    if (c) {                                             // shift right by 1
-      const uint32_t lost = Z[0] & 1u;
-#pragma unroll
-      for (int i = 0; i < L; ++i) Z[i] = __funnelshift_r(Z[i], Z[i + 1], 1);
-      Z[L] = (Z[L] >> 1) | 0x80000000u;
-      stk |= lost;
-      e = eb + 1;
-    } else {
-      e = eb;
-    }
-  } else {
-    uint32_t bw = stk != 0u ? 1u : 0u;                 // X - Y - [sticky]
-#pragma unroll
-    for (int i = 0; i <= L; ++i) {
-      uint64_t tt = (uint64_t)X[i] - Y[i] - bw;
-      Z[i] = (uint32_t)tt;
-      bw = (uint32_t)(tt >> 63);
-    }
-    uint32_t any = 0u;
-#pragma unroll
-    for (int i = 0; i <= L; ++i) any |= Z[i];
-    if (any == 0u) { s.set_zero(); return; }            // exact cancellation: +0
-    const uint32_t lz = clz_limbs<L + 1>(Z);
-    shl_bits<L + 1>(Z, lz);
     e = eb - (int32_t)lz;
+  } else {
+    // ---- far path (d >= 2, or same sign): align small, add/sub, <= 1-bit norm
+    shr_bits_sticky<L + 1>(Y, d, stk);
+    if (same) {
+      const uint32_t c = add_n<L + 1>(Z, Z, Y);
+      stk |= Z[0] & c;                                   // bit lost by the 1-bit shift
+#pragma unroll
+      for (int i = 0; i < L; ++i) Z[i] = __funnelshift_r(Z[i], Z[i + 1], c);
+      Z[L] = __funnelshift_r(Z[L], c, c);
+      e = eb + (int32_t)c;
+    } else {
+      sub_n<L + 1>(Z, Z, Y, stk != 0u ? 1u : 0u);       // X - Y - [sticky]
+      const uint32_t sh = (~Z[L]) >> 31;                // top bit clear -> shift 1
+#pragma unroll
+      for (int i = L; i > 0; --i) Z[i] = __funnelshift_l(Z[i - 1], Z[i], sh);
+      Z[0] <<= sh;
+      e = eb - (int32_t)sh;
+    }
   }
-  rb = Z[0] >> 31;
-  st = stk | (Z[0] << 1);
+  const uint32_t rb = Z[0] >> 31;
+  const uint32_t st = stk | (Z[0] << 1);
 #pragma unroll
   for (int i = 0; i < L; ++i) s.m[i] = Z[i + 1];
   const uint32_t cy = rne_increment<L>(s.m, rb, st);

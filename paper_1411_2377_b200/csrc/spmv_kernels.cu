@@ -94,36 +94,36 @@ __global__ void __launch_bounds__(128) spmv_sell(PartView P, XView x, YView y) {
 
   MP<L> s;
   s.set_zero();
-  if (len > 0) {
-    // software pipeline: entry j+1's loads in flight during entry j's math
-    int64_t g = g0;
-    int col = __ldg(P.col + g * 32 + l);
-    int32_t w = __ldg(P.expw + g * 32 + l);
-    uint32_t a[L], xv[L];
-    load_a<L>(P.limbs, g, l, a);
+  // Two register buffers (ping-pong, no copies): entry j+1's loads are in
+  // flight while entry j's product and add run.
+  uint32_t a0[L], x0[L], a1[L], x1[L];
+  int32_t w0 = 0, w1 = 0, e0 = 0, e1 = 0;
+  uint32_t s0 = 0, s1 = 0;
+  const int32_t* colp = P.col + g0 * 32 + l;
+  const int32_t* expp = P.expw + g0 * 32 + l;
+  auto fetch = [&](int j, uint32_t (&a)[L], uint32_t (&xv)[L], int32_t& w, int32_t& ex,
+                   uint32_t& sx) {
+    const int col = __ldg(colp + 32 * j);
+    w = __ldg(expp + 32 * j);
+    load_a<L>(P.limbs, g0 + j, l, a);
     load_x<L>(x.limbs, col, xv);
-    int32_t ex = __ldg(x.exps + col);
-    uint32_t sx = __ldg(x.signs + col);
-    for (int j = 0; j < len; ++j) {
-      uint32_t ca[L], cx[L];
-#pragma unroll
-      for (int i = 0; i < L; ++i) { ca[i] = a[i]; cx[i] = xv[i]; }
-      const int32_t cw = w, cex = ex;
-      const uint32_t csx = sx;
-      if (j + 1 < len) {
-        ++g;
-        col = __ldg(P.col + g * 32 + l);
-        w = __ldg(P.expw + g * 32 + l);
-        load_a<L>(P.limbs, g, l, a);
-        load_x<L>(x.limbs, col, xv);
-        ex = __ldg(x.exps + col);
-        sx = __ldg(x.signs + col);
-      }
-      MP<L> t;
-      const int32_t ea = (int32_t)((uint32_t)cw << 1) >> 1;
-      mp_mul<L>(ca, ea, (uint32_t)cw >> 31, cx, cex, csx, t);
-      mp_add<L>(s, t);
-    }
+    ex = __ldg(x.exps + col);
+    sx = __ldg(x.signs + col);
+  };
+  auto step = [&](const uint32_t (&a)[L], const uint32_t (&xv)[L], int32_t w, int32_t ex,
+                  uint32_t sx) {
+    MP<L> t;
+    const int32_t ea = (int32_t)((uint32_t)w << 1) >> 1;
+    mp_mul<L>(a, ea, (uint32_t)w >> 31, xv, ex, sx, t);
+    mp_add<L>(s, t);
+  };
+  if (len > 0) fetch(0, a0, x0, w0, e0, s0);
+  for (int j = 0; j < len; j += 2) {
+    if (j + 1 < len) fetch(j + 1, a1, x1, w1, e1, s1);
+    step(a0, x0, w0, e0, s0);
+    if (j + 1 >= len) break;
+    if (j + 2 < len) fetch(j + 2, a0, x0, w0, e0, s0);
+    step(a1, x1, w1, e1, s1);
   }
   store_y<L>(y, row, s);
 }
