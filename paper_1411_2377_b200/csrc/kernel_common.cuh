@@ -1,0 +1,74 @@
+// kernel_common.cuh - load/store helpers shared by the SpMV kernels
+// (layout.h describes the device layout).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "layout.h"
+#include "mp_device.cuh"
+
+namespace mpsp {
+
+template <int L>
+struct Chunk;  // CW-word vector type
+template <> struct Chunk<1> { using T = uint32_t; static constexpr int CW = 1; };
+template <> struct Chunk<2> { using T = uint2; static constexpr int CW = 2; };
+template <int L> struct Chunk { using T = uint4; static constexpr int CW = 4; };
+
+__device__ __forceinline__ void unpack_chunk(uint32_t v, uint32_t* d) { d[0] = v; }
+__device__ __forceinline__ void unpack_chunk(const uint2& v, uint32_t* d) { d[0] = v.x; d[1] = v.y; }
+__device__ __forceinline__ void unpack_chunk(const uint4& v, uint32_t* d) {
+  d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+}
+
+// A entry limbs of group g, lane l.
+template <int L>
+__device__ __forceinline__ void load_a(const uint32_t* __restrict__ limbs, int64_t g, int l,
+                                       uint32_t (&a)[L]) {
+  using C = Chunk<L>;
+  constexpr int NC = L / C::CW;
+  const typename C::T* base = reinterpret_cast<const typename C::T*>(limbs) + g * NC * 32 + l;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    typename C::T v = __ldg(base + c * 32);
+    unpack_chunk(v, &a[c * C::CW]);
+  }
+}
+
+// x element `col` (element-major limbs).
+template <int L>
+__device__ __forceinline__ void load_x(const uint32_t* __restrict__ xl, int col, uint32_t (&x)[L]) {
+  using C = Chunk<L>;
+  constexpr int NC = L / C::CW;
+  const typename C::T* base = reinterpret_cast<const typename C::T*>(xl) + (int64_t)col * NC;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    typename C::T v = __ldg(base + c);
+    unpack_chunk(v, &x[c * C::CW]);
+  }
+}
+
+template <int L>
+__device__ __forceinline__ void store_y(const YView& y, int row, const MP<L>& s) {
+  using C = Chunk<L>;
+  constexpr int NC = L / C::CW;
+  typename C::T* base = reinterpret_cast<typename C::T*>(y.limbs) + (int64_t)row * NC;
+  const bool z = s.is_zero();
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    typename C::T v;
+    if constexpr (C::CW == 1) {
+      v = s.m[c];
+    } else if constexpr (C::CW == 2) {
+      v = make_uint2(s.m[2 * c], s.m[2 * c + 1]);
+    } else {
+      v = make_uint4(s.m[4 * c], s.m[4 * c + 1], s.m[4 * c + 2], s.m[4 * c + 3]);
+    }
+    base[c] = v;
+  }
+  y.exps[row] = z ? 0 : s.e;
+  y.signs[row] = z ? (uint8_t)0 : (uint8_t)s.s;
+}
+
+}  // namespace mpsp

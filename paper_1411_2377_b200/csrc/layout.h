@@ -29,6 +29,9 @@ struct PartView {
   const uint32_t* limbs;      // [nentries * L]
   int64_t nslots;             // 32 * nslices
   int64_t nslices;
+  int64_t nlong;              // slices [0, nlong) hold rows longer than the
+                              // long-row threshold (spmv_long); the rest
+                              // go to spmv_sell
 };
 
 struct XView {
@@ -45,6 +48,12 @@ struct YView {
 
 // Launch the SpMV over one part on `stream`; returns a cudaError_t value.
 int launch_spmv(int L, const PartView& P, const XView& x, const YView& y, void* stream);
+// Long-row kernel over slices [0, P.nlong); returns a cudaError_t value.
+int launch_spmv_long(int L, const PartView& P, const XView& x, const YView& y, void* stream);
+// Row-length threshold above which a slice goes to the long-row kernel.
+int long_row_threshold();
+// Launch counter increment (shared by the kernel files).
+void launch_counter_add(int64_t k);
 // Integer-MAC microbenchmark (roofline denominator); returns cudaError_t.
 int run_imad_bench(double out[3]);
 // Launches this process has made.

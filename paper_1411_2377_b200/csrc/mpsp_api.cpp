@@ -52,7 +52,7 @@ void parallel_for(int64_t n, F f) {
 }
 
 struct DevPart {
-  int64_t nrows = 0, nnz = 0, nslices = 0, nentries = 0;
+  int64_t nrows = 0, nnz = 0, nslices = 0, nentries = 0, nlong = 0;
   int32_t max_len = 0;
   int64_t* slice_ptr = nullptr;
   int32_t* slot_row = nullptr;
@@ -66,7 +66,7 @@ struct DevPart {
     PartView v;
     v.slice_ptr = slice_ptr; v.slot_row = slot_row; v.slot_len = slot_len;
     v.col = col; v.expw = expw; v.limbs = limbs;
-    v.nslices = nslices; v.nslots = nslices * 32;
+    v.nslices = nslices; v.nslots = nslices * 32; v.nlong = nlong;
     return v;
   }
   void release() {
@@ -137,6 +137,12 @@ int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32
   }
   const int64_t nent = sp[(size_t)nslices];
   P.nentries = nent;
+  {
+    const int64_t T = long_row_threshold();
+    int64_t nl = 0;
+    while (nl < nslices && (sp[(size_t)nl + 1] - sp[(size_t)nl]) / 32 > T) ++nl;
+    P.nlong = nl;
+  }
   const int CW = L < 4 ? L : 4, NC = L / CW;
   // --- a1: repack (host), zero-filled padding
   std::vector<int32_t> hcol, hexp;
@@ -270,7 +276,9 @@ int do_spmv(const mpsp_csr* A, bool transpose, const uint32_t* xl, const int32_t
   const DevPart& P = transpose ? A->T : A->A;
   XView xv{xl, xe, xs};
   YView yv{yl, ye, ys};
-  int err = launch_spmv(L, P.view(), xv, yv, stream);
+  int err = launch_spmv_long(L, P.view(), xv, yv, stream);
+  if (err != 0) return cuda_fail((cudaError_t)err);
+  err = launch_spmv(L, P.view(), xv, yv, stream);
   if (err != 0) return cuda_fail((cudaError_t)err);
   return MPSP_OK;
 }

@@ -79,3 +79,30 @@ def test_config_recipes_other_precisions(cfg, p):
     n = {"C1": 1000, "C3": 3000, "C5": 2500}[cfg]
     d = gen.make(cfg, n=n, p=p, seed=3)
     assert_same(gpu_run(d, "ax"), oracle_full(d, "ax"), f"{cfg} p={p}")
+
+
+@pytest.fixture
+def all_rows_long(monkeypatch):
+    """Route every row (length > 0) through the long-row kernel."""
+    monkeypatch.setenv("MPSP_LONG_T", "0")
+
+
+@pytest.mark.parametrize("p", PS)
+def test_long_row_kernel_stress(p, all_rows_long):
+    d = gen.stress(p, seed=4)
+    for op in ("ax", "atx"):
+        assert_same(gpu_run(d, op), oracle_full(d, op), f"long-kernel stress p={p} {op}")
+
+
+@pytest.mark.parametrize("cfg,n", [("C1", None), ("C3", 6000), ("C4", 20_000), ("C5", 4900)])
+def test_long_row_kernel_configs(cfg, n, all_rows_long):
+    d = gen.make(cfg, n=n, seed=6)
+    assert_same(gpu_run(d, "ax"), oracle_full(d, "ax"), f"long-kernel {cfg}")
+
+
+@pytest.mark.parametrize("thr", ["8", "31", "200"])
+def test_long_threshold_split_c4(thr, monkeypatch):
+    monkeypatch.setenv("MPSP_LONG_T", thr)
+    d = gen.make("C4", n=20_000, seed=8)
+    for op in ("ax", "atx"):
+        assert_same(gpu_run(d, op), oracle_full(d, op), f"C4 threshold {thr} {op}")
