@@ -2,24 +2,34 @@
 // part 2: the ordered add chain of a 5000-long row is a serial critical path).
 //
 // One CTA owns LR = 8 consecutive length-sorted rows (a quarter of a SELL
-// slice).  Warp 0 is the CONSUMER: lane r runs row r's chain
+// slice).  One warp is the CONSUMER: lane r runs row r's chain
 //     s = RN(s + t_j),  j ascending.
-// Warps 1..LPW are PRODUCERS: for positions in chunks of LC they compute the
-// rounded products t_j = RN(a_j * x[col_j]) (Comba, IMAD.WIDE) and PRE-ALIGN
-// them to the consumer's published accumulator exponent E_s (speculation:
-// E_s changes in well under 1% of the steps of a long row).  A pre-aligned
-// slot holds Y = |t| * 2^32 >> (E_s - E_t) as L+1 limbs (one guard limb) plus
-// a sticky flag.  The consumer's fast step is then one (L)-limb carry chain:
-//     R = S + Q(Y) + cin,   cin = complement carry + RNE increment,
-// valid while the result stays in S's binade.  Everything else is exact
-// fallback, never approximation:
-//   * E_used != E_s (stale speculation): realign Y by |delta| <= 31 bits
-//     (right: bits go to sticky; left, when adding or when the sticky tail is
-//     empty: exact for rounding, since only the round bit and "anything
-//     below" matter and both stay known);
-//   * binade change (carry out / top bit lost) or |delta| > 31 or S == 0
-//     without an exact slot: the step is recomputed from S (restored by
-//     subtracting back) and the product reloaded, with the general mp_add.
+// The other LPW warps are PRODUCERS: for positions in chunks of LC they
+// compute the rounded products t_j = RN(a_j * x[col_j]) (Comba, IMAD.WIDE)
+// and PRE-ALIGN them against the consumer's published accumulator tag
+// (E_s, sign_s) - a speculation, since E_s changes in about 1% of the steps
+// of a long row.  For that tag the producer also forms the two's complement
+// (opposite signs) and the round-to-nearest-even decision of the step, which
+// only depends on the product once the accumulator's binade is fixed:
+//     Q = +-(|t| * 2^32 >> (E_s - E_t))  (L+1 limbs, guard limb q0),
+//     cin = c0 + [round up] + [tie] * lsb(S + Q),
+// so the consumer's fast step is   S := S + Q_up + cin   in S's binade.
+//
+// The consumer keeps S in CARRY-SAVE form (limbs A_i plus one pending carry
+// C_i per limb; carries out of the top limb are dropped, i.e. arithmetic is
+// mod 2^(32L), which is exact while S stays in [2^(32L-1), 2^(32L))): a step
+// is 2 independent ops per limb instead of an L-deep carry chain.  The lowest
+// limb never has a pending carry, so the tie LSB is exact; the binade is
+// checked conservatively on the top limb (true top in {T, T+1}).
+//
+// Everything outside the fast path is exact fallback, never approximation,
+// handled in one warp-uniform rare block: stale tag (realign by <= 31 bits:
+// right shifts feed the sticky; a left shift keeps the round bit, and a
+// subtracted sticky tail < 2^r borrows exactly like the "-1" of the sticky
+// trick because the low r bits are zero), zero accumulator, binade margin
+// violated, or a binade change: S is restored exactly (resolve carries,
+// subtract the step back) and the step redone with the general mp_add on the
+// raw product kept in the slot.
 // Chunks are double-buffered in shared memory; one __syncthreads per chunk.
 #include <cuda_runtime.h>
 
@@ -37,13 +47,43 @@ constexpr int LPW = 3;                     // producer warps
 constexpr int LTHREADS = 32 * (1 + LPW);
 constexpr int LPROD_PER_LANE = LR * LC / (32 * LPW);   // = 2
 static_assert(LR * LC == 32 * LPW * LPROD_PER_LANE, "chunk must tile the producers");
-constexpr int32_t KEY_UNKNOWN = INT_MIN;
+constexpr int32_t E_UNKNOWN = INT_MIN;
 
-enum : uint32_t { F_SIGN = 1u, F_STK = 2u, F_ZERO = 4u, F_EXACT = 8u };
+#ifdef MPSP_LONG_PROFILE
+// debug build only: per-chunk timestamps of CTA 0 (producer role 1 lane 0,
+// consumer lane 0): [chunk][0..3] = prod start, prod end, cons start, cons end
+__device__ long long g_long_prof[4096][4];
+#define LPROF(c, k) do { if (blockIdx.x == 0 && (c) < 4096) g_long_prof[c][k] = clock64(); } while (0)
+#else
+#define LPROF(c, k) do { } while (0)
+#endif
 
+#ifdef MPSP_LONG_CHECK
+// debug build only: first divergence between the fast/rare consumer and a
+// reference chain (general mp_add of the raw products) - diagnostics
+__device__ unsigned long long g_long_chk[64];
+__device__ int g_long_chk_flag;
+#endif
+
+// info word bits
+enum : uint32_t {
+  I_C0 = 1u, I_INC = 2u, I_TIE = 4u, I_ZERO = 8u, I_OPP = 16u, I_STK = 32u, I_SIGNT = 64u,
+  I_SU = 128u,
+  // exponent gap 0: |Q| may reach 2^(32L), so a wrap mod 2^(32L) would not be
+  // visible on the top limb -> always take the exact path
+  I_RARE = 256u
+};
+
+// Slot (one product of one row).  Part A (read every step, 128-bit loads):
+// Q_up[0..L-1], info, E_used.  Part B (rare path): q0, M[0..L-1], E_t.
 template <int L>
 struct LongSlot {
-  static constexpr int W = L + 3;          // Y[0..L], flags, E_used  (odd stride for even L)
+  static constexpr int A = (L + 2 + 3) / 4 * 4;
+  static constexpr int B = (L + 2 + 3) / 4 * 4;
+  static constexpr int W0 = A + B;
+  static constexpr int W = ((W0 / 4) % 2 == 1) ? W0 : W0 + 4;   // odd # of 16B -> no conflicts
+  static constexpr int QU = 0, INFO = L, EU = L + 1;
+  static constexpr int Q0 = A, M = A + 1, ET = A + 1 + L;
 };
 
 // Read at every mpsp_csr_create (tests lower it to route all rows through
@@ -54,237 +94,390 @@ int long_row_threshold() {
 }
 
 template <int L>
+struct Entry {
+  uint32_t a[L], x[L];
+  int32_t w, ex;
+  uint32_t sx;
+};
+
+template <int L>
 __device__ __forceinline__ void load_entry(const PartView& P, const XView& x, int64_t g, int l,
-                                           uint32_t (&a)[L], int32_t& w, uint32_t (&xv)[L],
-                                           int32_t& ex, uint32_t& sx) {
+                                           bool valid, Entry<L>& E) {
+  if (!valid) {
+#pragma unroll
+    for (int i = 0; i < L; ++i) { E.a[i] = 0u; E.x[i] = 0u; }
+    E.w = 0; E.ex = 0; E.sx = 0u;
+    return;
+  }
   const int col = __ldg(P.col + g * 32 + l);
-  w = __ldg(P.expw + g * 32 + l);
-  load_a<L>(P.limbs, g, l, a);
-  load_x<L>(x.limbs, col, xv);
-  ex = __ldg(x.exps + col);
-  sx = __ldg(x.signs + col);
+  E.w = __ldg(P.expw + g * 32 + l);
+  load_a<L>(P.limbs, g, l, E.a);
+  load_x<L>(x.limbs, col, E.x);
+  E.ex = __ldg(x.exps + col);
+  E.sx = __ldg(x.signs + col);
 }
 
+// Producer: t = RN(a*x), then its slot against the tag (ek, sk).
 template <int L>
-__device__ __forceinline__ void product_of(const uint32_t (&a)[L], int32_t w, const uint32_t (&xv)[L],
-                                           int32_t ex, uint32_t sx, MP<L>& t) {
-  const int32_t ea = (int32_t)((uint32_t)w << 1) >> 1;
-  mp_mul<L>(a, ea, (uint32_t)w >> 31, xv, ex, sx, t);
-}
-
-// Producer: turn t into a slot aligned to `key` (the consumer's E_s).
-template <int L>
-__device__ __forceinline__ void write_slot(uint32_t* slot, const MP<L>& t, bool valid, int32_t key) {
+__device__ __forceinline__ void produce_slot(uint32_t* slot, const Entry<L>& E, bool valid,
+                                             int32_t ek, uint32_t sk) {
+  using SL = LongSlot<L>;
+  MP<L> t;
+  const int32_t ea = (int32_t)((uint32_t)E.w << 1) >> 1;
+  mp_mul<L>(E.a, ea, (uint32_t)E.w >> 31, E.x, E.ex, E.sx, t);
+  const bool zero = !valid || t.is_zero();
   uint32_t Y[L + 1];
   Y[0] = 0u;
 #pragma unroll
   for (int i = 0; i < L; ++i) Y[i + 1] = t.m[i];
-  uint32_t fl, stk = 0u;
+  int64_t d = (int64_t)ek - (int64_t)t.e;
   int32_t eu;
-  const bool zero = !valid || t.is_zero();
-  int64_t d = (int64_t)key - (int64_t)t.e;
-  if (zero) {
-    fl = F_ZERO;
-    eu = 0;
+  uint32_t su;
+  if (ek == E_UNKNOWN || d < 0) {          // exact form w.r.t. its own exponent
     d = 0;
-  } else if (key == KEY_UNKNOWN || d < 0) {
-    fl = F_EXACT | t.s;                    // exact copy of t (d = 0 w.r.t. its own exponent)
     eu = t.e;
-    d = 0;
+    su = t.s;
   } else {
     if (d > 32 * (L + 1)) d = 32 * (L + 1);
-    fl = t.s | (d == 0 ? F_EXACT : 0u);
-    eu = key;
+    eu = ek;
+    su = sk;
   }
+  uint32_t stk = 0u;
   shr_bits_sticky<L + 1>(Y, (uint32_t)d, stk);
-  if (stk) fl |= F_STK;
+  stk = stk ? 1u : 0u;
+  const uint32_t opp = t.s ^ su;
+  const uint32_t mask = 0u - opp;
+  const uint32_t c0 = opp & ((Y[0] == 0u) ? 1u : 0u) & (stk ^ 1u);
+  const uint32_t q0 = (Y[0] ^ mask) + (opp & (stk ^ 1u));
+  const uint32_t rb = q0 >> 31;
+  const uint32_t st = (q0 << 1) | stk;
+  const uint32_t inc = rb & (st != 0u ? 1u : 0u);
+  const uint32_t tie = rb & (st == 0u ? 1u : 0u);
+  uint32_t info = c0 | (inc << 1) | (tie << 2) | (opp << 4) | (stk << 5) | (t.s << 6) | (su << 7) |
+                  (d == 0 ? I_RARE : 0u);
+  if (zero) info = I_ZERO;
 #pragma unroll
-  for (int i = 0; i <= L; ++i) slot[i] = zero ? 0u : Y[i];
-  slot[L + 1] = fl;
-  slot[L + 2] = (uint32_t)eu;
+  for (int i = 0; i < L; ++i) slot[SL::QU + i] = zero ? 0u : (Y[i + 1] ^ mask);
+  slot[SL::INFO] = info;
+  slot[SL::EU] = (uint32_t)eu;
+  slot[SL::Q0] = q0;
+#pragma unroll
+  for (int i = 0; i < L; ++i) slot[SL::M + i] = t.m[i];
+  slot[SL::ET] = (uint32_t)t.e;
+}
+
+template <int L>
+struct ProdPrefetch { static constexpr bool on = (L <= 8); };
+
+// Consumer rare path: exact handling of one step from the exact accumulator
+// S (value before the step) and the slot.
+template <int L>
+__device__ __forceinline__ void exact_step(MP<L>& S, const uint32_t* sl, const uint32_t* qu,
+                                           uint32_t info, int32_t eu) {
+  using SL = LongSlot<L>;
+  if (info & I_ZERO) return;
+  const uint32_t st_sign = (info >> 6) & 1u;
+  if (S.is_zero()) {
+#pragma unroll
+    for (int i = 0; i < L; ++i) S.m[i] = sl[SL::M + i];
+    S.e = (int32_t)sl[SL::ET];
+    S.s = st_sign;
+    return;
+  }
+  // recover the aligned magnitude Y (L+1 limbs) and the sticky flag
+  const uint32_t stk0 = (info >> 5) & 1u;
+  uint32_t Y[L + 1];
+  Y[0] = sl[SL::Q0];
+#pragma unroll
+  for (int i = 0; i < L; ++i) Y[i + 1] = qu[i];
+  if (info & I_OPP) {
+    // stored: q0 = ~Y0 + 1 - stk (mod 2^32), Q_up = ~Y_up (the carry c0 of
+    // the full complement travels separately in cin)
+    Y[0] = 0u - Y[0] - stk0;
+#pragma unroll
+    for (int i = 1; i <= L; ++i) Y[i] = ~Y[i];
+  }
+  uint32_t stk = stk0;
+  bool general = false;
+  const int64_t delta = (int64_t)S.e - (int64_t)eu;
+  if (delta > 0 && delta <= 31) {
+    const uint32_t r = (uint32_t)delta;
+    stk |= (Y[0] << (32u - r)) != 0u ? 1u : 0u;
+#pragma unroll
+    for (int i = 0; i < L; ++i) Y[i] = __funnelshift_r(Y[i], Y[i + 1], r);
+    Y[L] >>= r;
+  } else if (delta < 0 && delta >= -31 && __clz(Y[L]) >= (int)(-delta)) {
+    const uint32_t r = (uint32_t)(-delta);
+#pragma unroll
+    for (int i = L; i > 0; --i) Y[i] = __funnelshift_l(Y[i - 1], Y[i], r);
+    Y[0] <<= r;
+  } else if (delta != 0) {
+    general = true;
+  }
+  if (!general) {
+    const uint32_t opp = st_sign ^ S.s;
+    const uint32_t mask = 0u - opp;
+    const uint32_t c0 = opp & ((Y[0] == 0u) ? 1u : 0u) & (stk ^ 1u);
+    const uint32_t q0 = (Y[0] ^ mask) + (opp & (stk ^ 1u));
+    uint32_t Q[L];
+#pragma unroll
+    for (int i = 0; i < L; ++i) Q[i] = Y[i + 1] ^ mask;
+    const uint32_t rb = q0 >> 31;
+    const uint32_t st = (q0 << 1) | stk;
+    const uint32_t lsb = (S.m[0] ^ Q[0] ^ c0) & 1u;
+    const uint32_t inc = rb & ((st != 0u) | lsb);
+    uint32_t R[L];
+    uint32_t co = add_n<L>(R, S.m, Q);
+    co += inc_n<L>(R, c0);
+    co += inc_n<L>(R, inc);
+    const bool bad = opp ? ((co == 0u) || (R[L - 1] < 0x80000000u) ||
+                            (R[L - 1] == 0x80000000u && inc))
+                         : (co != 0u);
+    if (!bad) {
+#pragma unroll
+      for (int i = 0; i < L; ++i) S.m[i] = R[i];
+      return;
+    }
+  }
+  MP<L> t;                                  // general add of the raw product
+#pragma unroll
+  for (int i = 0; i < L; ++i) t.m[i] = sl[SL::M + i];
+  t.e = (int32_t)sl[SL::ET];
+  t.s = st_sign;
+  mp_add<L>(S, t);
 }
 
 template <int L>
 __global__ void __launch_bounds__(LTHREADS) spmv_long(PartView P, XView x, YView y) {
   extern __shared__ uint32_t smem[];
-  constexpr int SW = LongSlot<L>::W;
+  using SL = LongSlot<L>;
+  constexpr int SW = SL::W;
   uint32_t* buf = smem;                                          // [2][LC][LR][SW]
-  volatile int32_t* es_pub = (volatile int32_t*)(smem + 2 * LC * LR * SW);
+  // published tag per row: low 32 bits E_s, high 32 bits sign_s (one 64-bit word)
+  volatile unsigned long long* key_pub = (volatile unsigned long long*)(smem + 2 * LC * LR * SW);
   const int64_t s = blockIdx.x >> 2;
   const int sub = blockIdx.x & 3;
   const int64_t slot0 = s * 32 + sub * LR;
   const int64_t g0 = P.slice_ptr[s] >> 5;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // the consumer role rotates over the CTA's warps so that consumers of
+  // co-resident CTAs spread over the SM's four schedulers
+  const int cw = (int)(blockIdx.x & 3);
+  const int hw = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = (hw - cw + 4) & 3;                            // role: 0 = consumer
   const int width = P.slot_len[slot0];                           // longest row (sorted)
-  if (threadIdx.x < LR) es_pub[threadIdx.x] = KEY_UNKNOWN;
+  if (threadIdx.x < LR) key_pub[threadIdx.x] = (unsigned long long)(uint32_t)E_UNKNOWN;
   __syncthreads();
   const int nchunks = (width + LC - 1) / LC;
 
-  // ---- consumer state (warp 0, lanes < LR)
-  MP<L> S;
-  S.set_zero();
+  // ---- consumer state (role 0, lanes < LR): S in carry-save form
   const bool cons = (warp == 0 && lane < LR);
-  // ---- producer constants (warps 1..LPW): row r = lane % LR, positions jj
+  uint32_t Acs[L], Ccs[L];                 // limbs and pending carries (Ccs[0] unused)
+#pragma unroll
+  for (int i = 0; i < L; ++i) { Acs[i] = 0u; Ccs[i] = 0u; }
+  int32_t Ecur = E_UNKNOWN;
+  uint32_t Scur = 0u;
+  bool szero = true;
+#ifdef MPSP_LONG_CHECK
+  MP<L> Sref;
+  Sref.set_zero();
+#endif
+  // ---- producer constants: row r = lane % LR, positions jj
   const int pr = lane % LR;
   const int pbase = ((warp - 1) * 32 + lane) / LR;               // jj for u = 0
   const int prowlen = (warp > 0) ? P.slot_len[slot0 + pr] : 0;
+  constexpr int JSTEP = 32 * LPW / LR;
+  Entry<L> pre[ProdPrefetch<L>::on ? LPROD_PER_LANE : 1];
+  if (ProdPrefetch<L>::on && warp > 0 && nchunks > 0) {
+#pragma unroll
+    for (int u = 0; u < LPROD_PER_LANE; ++u) {
+      const int j = pbase + u * JSTEP;
+      load_entry<L>(P, x, g0 + j, sub * LR + pr, j < prowlen, pre[u]);
+    }
+  }
 
   for (int c = 0; c <= nchunks; ++c) {
     if (warp > 0 && c < nchunks) {
+      if (warp == 1 && lane == 0) LPROF(c, 0);
       uint32_t* B = buf + (c & 1) * (LC * LR * SW);
-      const int32_t key = es_pub[pr];
-      uint32_t a[LPROD_PER_LANE][L], xv[LPROD_PER_LANE][L];
-      int32_t w[LPROD_PER_LANE], ex[LPROD_PER_LANE];
-      uint32_t sx[LPROD_PER_LANE];
-      bool valid[LPROD_PER_LANE];
+      const unsigned long long kw = key_pub[pr];
+      const int2 key = make_int2((int32_t)(uint32_t)kw, (int32_t)(kw >> 32));
+      if constexpr (ProdPrefetch<L>::on) {
+        Entry<L> cur[LPROD_PER_LANE];
 #pragma unroll
-      for (int u = 0; u < LPROD_PER_LANE; ++u) {
-        const int jj = pbase + u * (32 * LPW / LR);
-        const int j = c * LC + jj;
-        valid[u] = j < prowlen;
-        if (valid[u]) {
-          load_entry<L>(P, x, g0 + j, sub * LR + pr, a[u], w[u], xv[u], ex[u], sx[u]);
-        } else {
+        for (int u = 0; u < LPROD_PER_LANE; ++u) cur[u] = pre[u];
+        if (c + 1 < nchunks) {
 #pragma unroll
-          for (int i = 0; i < L; ++i) { a[u][i] = 0u; xv[u][i] = 0u; }
-          w[u] = 0; ex[u] = 0; sx[u] = 0u;
+          for (int u = 0; u < LPROD_PER_LANE; ++u) {
+            const int j = (c + 1) * LC + pbase + u * JSTEP;
+            load_entry<L>(P, x, g0 + j, sub * LR + pr, j < prowlen, pre[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < LPROD_PER_LANE; ++u) {
+          const int jj = pbase + u * JSTEP;
+          produce_slot<L>(B + (jj * LR + pr) * SW, cur[u], c * LC + jj < prowlen, key.x,
+                          (uint32_t)key.y);
+        }
+      } else {
+        Entry<L> cur[LPROD_PER_LANE];
+#pragma unroll
+        for (int u = 0; u < LPROD_PER_LANE; ++u) {
+          const int j = c * LC + pbase + u * JSTEP;
+          load_entry<L>(P, x, g0 + j, sub * LR + pr, j < prowlen, cur[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < LPROD_PER_LANE; ++u) {
+          const int jj = pbase + u * JSTEP;
+          produce_slot<L>(B + (jj * LR + pr) * SW, cur[u], c * LC + jj < prowlen, key.x,
+                          (uint32_t)key.y);
         }
       }
-#pragma unroll
-      for (int u = 0; u < LPROD_PER_LANE; ++u) {
-        const int jj = pbase + u * (32 * LPW / LR);
-        MP<L> t;
-        product_of<L>(a[u], w[u], xv[u], ex[u], sx[u], t);
-        write_slot<L>(B + (jj * LR + pr) * SW, t, valid[u], key);
-      }
+      if (warp == 1 && lane == 0) LPROF(c, 1);
     }
-    if (cons && c >= 1) {
+    if (warp == 0 && c >= 1) {
       const int cc = c - 1;
+      if (lane == 0) LPROF(cc, 2);
       const uint32_t* B = buf + (cc & 1) * (LC * LR * SW);
       const int jn = min(LC, width - cc * LC);
+      constexpr int NV = SL::A / 4;                       // 128-bit words of part A
+      const int ln = lane < LR ? lane : 0;                // idle lanes mirror lane 0
       for (int jj = 0; jj < jn; ++jj) {
-        const uint32_t* sl = B + (jj * LR + lane) * SW;
-        const uint32_t fl = sl[L + 1];
-        if (fl & F_ZERO) continue;
-        const int32_t eu = (int32_t)sl[L + 2];
-        uint32_t Y[L + 1];
+        const uint32_t* sl = B + (jj * LR + ln) * SW;
+#ifdef MPSP_LONG_CHECK
+        const int32_t dbg_E0 = Ecur;
+        const uint32_t dbg_S0 = Scur;
+        const bool dbg_z0 = szero;
+#endif
+        uint32_t Aw[NV * 4];
+        {
+          const uint4* v = reinterpret_cast<const uint4*>(sl);
 #pragma unroll
-        for (int i = 0; i <= L; ++i) Y[i] = sl[i];
-        uint32_t stk = (fl >> 1) & 1u;
-        const uint32_t st_sign = fl & F_SIGN;
-        bool slow = false;
-        if (S.is_zero()) {
-          if (fl & F_EXACT) {                       // S = t exactly
-#pragma unroll
-            for (int i = 0; i < L; ++i) S.m[i] = Y[i + 1];
-            S.e = eu;
-            S.s = st_sign;
-            es_pub[lane] = S.e;
-            continue;
-          }
-          slow = true;
-        } else {
-          const int64_t delta = (int64_t)S.e - (int64_t)eu;
-          if (delta > 0) {
-            if (delta <= 31) {                      // right: shifted-out bits -> sticky
-              const uint32_t r = (uint32_t)delta;
-              stk |= (Y[0] << (32u - r)) != 0u;
-#pragma unroll
-              for (int i = 0; i < L; ++i) Y[i] = __funnelshift_r(Y[i], Y[i + 1], r);
-              Y[L] >>= r;
-            } else {
-              slow = true;
-            }
-          } else if (delta < 0) {
-            // left: exact for round/sticky purposes when adding, or when no
-            // sticky bits exist (a subtracted sticky tail would borrow)
-            const uint32_t r = (uint32_t)(-delta);
-            const bool sub_with_stk = ((st_sign ^ S.s) != 0u) && stk;
-            if (r <= 31 && __clz(Y[L]) >= (int)r && !sub_with_stk) {
-#pragma unroll
-              for (int i = L; i > 0; --i) Y[i] = __funnelshift_l(Y[i - 1], Y[i], r);
-              Y[0] <<= r;
-            } else {
-              slow = true;
-            }
+          for (int q = 0; q < NV; ++q) {
+            const uint4 u4 = v[q];
+            Aw[4 * q] = u4.x; Aw[4 * q + 1] = u4.y; Aw[4 * q + 2] = u4.z; Aw[4 * q + 3] = u4.w;
           }
         }
-        if (!slow) {
-          // ---- fast step: R = S + Q + cin in S's binade
-          const uint32_t opp = st_sign ^ S.s;
-          uint32_t q0, c0;
-          if (opp) {                                // Q = -(Y + stk) mod 2^(32(L+1))
-            q0 = ~Y[0] + (1u - stk);
-            c0 = (Y[0] == 0u && stk == 0u) ? 1u : 0u;
+        const uint32_t info = Aw[SL::INFO];
+        const int32_t eu = (int32_t)Aw[SL::EU];
+        // ---- fast step, branch-free: carry-save S += Q_up + cin
+        const uint32_t c0 = info & I_C0;
+        const uint32_t lsb = (Acs[0] ^ Aw[SL::QU] ^ c0) & 1u;
+        const uint32_t cin = c0 + ((info >> 1) & 1u) + (((info >> 2) & 1u) & lsb);
+        uint32_t A1[L], C1[L];
+        C1[0] = 0u;
+        {
+          const uint64_t t0 = (uint64_t)Acs[0] + Aw[SL::QU] + cin;
+          A1[0] = (uint32_t)t0;
+          if (L > 1) C1[1] = (uint32_t)(t0 >> 32);
 #pragma unroll
-            for (int i = 1; i <= L; ++i) Y[i] = ~Y[i];
-          } else {
-            q0 = Y[0];
-            c0 = 0u;
+          for (int i = 1; i < L; ++i) {
+            const uint64_t ti = (uint64_t)Acs[i] + Aw[SL::QU + i] + Ccs[i];
+            A1[i] = (uint32_t)ti;
+            if (i + 1 < L) C1[i + 1] = (uint32_t)(ti >> 32);   // top carry dropped (mod 2^(32L))
           }
-          const uint32_t rb = q0 >> 31;
-          const uint32_t st = (q0 << 1) | stk;
-          const uint32_t lsb = (S.m[0] ^ Y[1] ^ c0) & 1u;
-          const uint32_t inc = rb & ((st != 0u) | lsb);
-          const uint32_t cin = c0 + inc;            // 0..2
-          uint32_t co;
+        }
+        const uint64_t T = (uint64_t)A1[L - 1] + (L > 1 ? C1[L - 1] : 0u);
+        const bool tag_ok = (eu == Ecur) && (((info >> 7) & 1u) == Scur) && !(info & I_RARE);
+        const bool safe = (T >= 0x80000001ull) && (T <= 0xFFFFFFFEull);
+        const bool zslot = (info & I_ZERO) != 0u;
+        const bool need = cons && (szero ? !zslot : !(safe && (zslot || tag_ok)));
+#pragma unroll
+        for (int i = 0; i < L; ++i) { Acs[i] = A1[i]; Ccs[i] = C1[i]; }
+        if (__any_sync(0xffffffffu, need)) {
+          if (need) {
+            // ---- rare path: restore the exact S before this step, redo exactly
+            MP<L> S;
+            if (szero) {
+              S.set_zero();
+            } else {
+              uint32_t R[L];
+              add_n<L>(R, Acs, Ccs);                 // resolve carries (mod 2^(32L))
+              uint32_t Qh[L];
+#pragma unroll
+              for (int i = 0; i < L; ++i) Qh[i] = Aw[SL::QU + i];
+              sub_n<L>(R, R, Qh, 0u);
+              uint32_t cv[L];
+              cv[0] = cin;
+#pragma unroll
+              for (int i = 1; i < L; ++i) cv[i] = 0u;
+              sub_n<L>(R, R, cv, 0u);
+#pragma unroll
+              for (int i = 0; i < L; ++i) S.m[i] = R[i];
+              S.e = Ecur;
+              S.s = Scur;
+            }
+            uint32_t qu[L];
+#pragma unroll
+            for (int i = 0; i < L; ++i) qu[i] = Aw[SL::QU + i];
+            exact_step<L>(S, sl, qu, info, eu);
+#pragma unroll
+            for (int i = 0; i < L; ++i) { Acs[i] = S.m[i]; Ccs[i] = 0u; }
+            szero = S.is_zero();
+            const int32_t Enew = szero ? E_UNKNOWN : S.e;
+            const uint32_t Snew = szero ? 0u : S.s;
+            if (Enew != Ecur || Snew != Scur)
+              key_pub[lane] = ((unsigned long long)Snew << 32) | (uint32_t)Enew;
+            Ecur = Enew;
+            Scur = Snew;
+          }
+        }
+#ifdef MPSP_LONG_CHECK
+        if (cons) {
           {
-            uint32_t dummy;
-            // carry flag := (cin >= 1); second unit of cin folded into limb 0
-            const uint32_t c1 = cin >> 1;
-            asm volatile("add.cc.u32 %0, %1, 0xffffffff;" : "=r"(dummy) : "r"(cin & 1u));
-            asm volatile("addc.cc.u32 %0, %0, %1;" : "+r"(S.m[0]) : "r"(Y[1]));
+            const uint32_t inf = Aw[SL::INFO];
+            if (!(inf & I_ZERO)) {
+              MP<L> t;
 #pragma unroll
-            for (int i = 1; i < L; ++i) asm volatile("addc.cc.u32 %0, %0, %1;" : "+r"(S.m[i]) : "r"(Y[i + 1]));
-            asm volatile("addc.u32 %0, 0, 0;" : "=r"(co));
-            if (c1) {                               // cin == 2 (complement carry + increment)
-              uint32_t co2 = inc_n<L>(S.m, 1u);
-              co += co2;
+              for (int i = 0; i < L; ++i) t.m[i] = sl[SL::M + i];
+              t.e = (int32_t)sl[SL::ET];
+              t.s = (inf >> 6) & 1u;
+              mp_add<L>(Sref, t);
             }
           }
-          bool bad;
-          if (opp) bad = (co == 0u) || (S.m[L - 1] < 0x80000000u) || (S.m[L - 1] == 0x80000000u && inc);
-          else bad = (co != 0u);
-          if (bad) {
-            // restore S: S = R - Q - cin (mod 2^(32L))
-            uint32_t Qh[L];
-#pragma unroll
-            for (int i = 0; i < L; ++i) Qh[i] = Y[i + 1];
-            sub_n<L>(S.m, S.m, Qh, 0u);
-            uint32_t cinv[L];
-            cinv[0] = cin;
-#pragma unroll
-            for (int i = 1; i < L; ++i) cinv[i] = 0u;
-            sub_n<L>(S.m, S.m, cinv, 0u);
-            slow = true;
+          MP<L> Sc;
+          add_n<L>(Sc.m, Acs, Ccs);
+          if (szero) Sc.set_zero();
+          bool diff = (Sc.is_zero() != Sref.is_zero());
+          if (!Sref.is_zero()) {
+            for (int i = 0; i < L; ++i) diff |= Sc.m[i] != Sref.m[i];
+            diff |= (Ecur != Sref.e) || (Scur != Sref.s);
           }
+          if (diff && atomicExch(&g_long_chk_flag, 1) == 0) {
+            g_long_chk[0] = blockIdx.x; g_long_chk[1] = lane; g_long_chk[2] = cc * LC + jj;
+            g_long_chk[3] = Aw[SL::INFO]; g_long_chk[4] = (uint32_t)Aw[SL::EU];
+            g_long_chk[5] = (uint32_t)dbg_E0; g_long_chk[6] = dbg_S0; g_long_chk[7] = dbg_z0;
+            g_long_chk[8] = (uint32_t)Ecur; g_long_chk[9] = Scur; g_long_chk[10] = (uint32_t)Sref.e;
+            g_long_chk[11] = Sref.s; g_long_chk[12] = sl[SL::Q0]; g_long_chk[13] = (uint32_t)sl[SL::ET];
+            for (int i = 0; i < L && i < 8; ++i) {
+              g_long_chk[16 + i] = Sc.m[i]; g_long_chk[24 + i] = Sref.m[i];
+              g_long_chk[32 + i] = Aw[SL::QU + i]; g_long_chk[40 + i] = sl[SL::M + i];
+            }
+          }
+          // continue from the reference to keep later checks meaningful
         }
-        if (slow) {
-          // ---- exact fallback: reload the entry, general product + add
-          const int j = cc * LC + jj;
-          uint32_t a[L], xv[L];
-          int32_t w, ex;
-          uint32_t sx;
-          load_entry<L>(P, x, g0 + j, sub * LR + lane, a, w, xv, ex, sx);
-          MP<L> t;
-          product_of<L>(a, w, xv, ex, sx, t);
-          mp_add<L>(S, t);
-          es_pub[lane] = S.is_zero() ? KEY_UNKNOWN : S.e;
-        }
+#endif
       }
+      if (lane == 0) LPROF(cc, 3);
     }
     __syncthreads();
   }
   if (cons) {
     const int row = P.slot_row[slot0 + lane];
-    if (row >= 0) store_y<L>(y, row, S);
+    if (row >= 0) {
+      MP<L> S;
+      add_n<L>(S.m, Acs, Ccs);
+      if (szero) S.set_zero();
+      S.e = Ecur;
+      S.s = Scur;
+      store_y<L>(y, row, S);
+    }
   }
 }
 
 template <int L>
 static int launch_long_L(const PartView& P, const XView& x, const YView& y, cudaStream_t st) {
   if (P.nlong <= 0) return 0;
-  const size_t smem = (size_t)(2 * LC * LR * LongSlot<L>::W + LR) * 4;
+  const size_t smem = (size_t)(2 * LC * LR * LongSlot<L>::W + 2 * LR) * 4;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(spmv_long<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -311,3 +504,15 @@ int launch_spmv_long(int L, const PartView& P, const XView& x, const YView& y, v
 }
 
 }  // namespace mpsp
+
+#ifdef MPSP_LONG_CHECK
+extern "C" int mpsp_debug_long_check(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, mpsp::g_long_chk, 64 * sizeof(unsigned long long));
+}
+#endif
+#ifdef MPSP_LONG_PROFILE
+extern "C" int mpsp_debug_long_profile(long long* out, int nchunks) {
+  if (nchunks > 4096) nchunks = 4096;
+  return (int)cudaMemcpyFromSymbol(out, mpsp::g_long_prof, (size_t)nchunks * 4 * sizeof(long long));
+}
+#endif
