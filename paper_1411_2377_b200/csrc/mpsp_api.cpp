@@ -86,6 +86,9 @@ struct mpsp_csr {
   uint32_t flags = 0;
   bool has_t = false;
   DevPart A, T;
+  // fork/join for running the long-row and short-row kernels concurrently
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // host-buffer API workspace (lazily allocated)
   cudaStream_t stream = nullptr;
   void* ws = nullptr;
@@ -276,9 +279,26 @@ int do_spmv(const mpsp_csr* A, bool transpose, const uint32_t* xl, const int32_t
   const DevPart& P = transpose ? A->T : A->A;
   XView xv{xl, xe, xs};
   YView yv{yl, ye, ys};
-  int err = launch_spmv_long(L, P.view(), xv, yv, stream);
+  const PartView pv = P.view();
+  const bool has_long = pv.nlong > 0, has_short = pv.nslots > pv.nlong * 32;
+  if (has_long && has_short && A->aux) {
+    // long rows on the aux stream (started first: they are the critical
+    // path), short rows on the caller's stream, joined back on the caller's
+    cudaStream_t us = (cudaStream_t)stream;
+    cudaError_t ce;
+    if ((ce = cudaEventRecord(A->ev_fork, us)) != cudaSuccess) return cuda_fail(ce);
+    if ((ce = cudaStreamWaitEvent(A->aux, A->ev_fork, 0)) != cudaSuccess) return cuda_fail(ce);
+    int err = launch_spmv_long(L, pv, xv, yv, A->aux);
+    if (err != 0) return cuda_fail((cudaError_t)err);
+    err = launch_spmv(L, pv, xv, yv, stream);
+    if (err != 0) return cuda_fail((cudaError_t)err);
+    if ((ce = cudaEventRecord(A->ev_join, A->aux)) != cudaSuccess) return cuda_fail(ce);
+    if ((ce = cudaStreamWaitEvent(us, A->ev_join, 0)) != cudaSuccess) return cuda_fail(ce);
+    return MPSP_OK;
+  }
+  int err = launch_spmv_long(L, pv, xv, yv, stream);
   if (err != 0) return cuda_fail((cudaError_t)err);
-  err = launch_spmv(L, P.view(), xv, yv, stream);
+  err = launch_spmv(L, pv, xv, yv, stream);
   if (err != 0) return cuda_fail((cudaError_t)err);
   return MPSP_OK;
 }
@@ -392,6 +412,14 @@ int mpsp_csr_create(mpsp_csr** out, int p_bits, int64_t n, const int64_t* rowptr
       rc = MPSP_E_NOMEM;
     }
   }
+  if (rc == MPSP_OK && (H->A.nlong > 0 || H->T.nlong > 0)) {
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    if ((ce = cudaStreamCreateWithPriority(&H->aux, cudaStreamNonBlocking, prio_hi)) != cudaSuccess ||
+        (ce = cudaEventCreateWithFlags(&H->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
+        (ce = cudaEventCreateWithFlags(&H->ev_join, cudaEventDisableTiming)) != cudaSuccess)
+      rc = cuda_fail(ce);
+  }
   if (rc == MPSP_OK) {
     ce = cudaDeviceSynchronize();
     if (ce != cudaSuccess) rc = cuda_fail(ce);
@@ -414,6 +442,9 @@ void mpsp_destroy(mpsp_csr* A) {
   A->T.release();
   if (A->ws) cudaFree(A->ws);
   if (A->stream) cudaStreamDestroy(A->stream);
+  if (A->aux) cudaStreamDestroy(A->aux);
+  if (A->ev_fork) cudaEventDestroy(A->ev_fork);
+  if (A->ev_join) cudaEventDestroy(A->ev_join);
   cudaSetDevice(cur);
   cudaGetLastError();
   delete A;

@@ -75,15 +75,16 @@ enum : uint32_t {
 };
 
 // Slot (one product of one row).  Part A (read every step, 128-bit loads):
-// Q_up[0..L-1], info, E_used.  Part B (rare path): q0, M[0..L-1], E_t.
+// Q_up[0..L-1], Y0 (magnitude guard limb), info, E_used.  Part B (rare
+// path): M[0..L-1] (raw rounded product mantissa), E_t.
 template <int L>
 struct LongSlot {
-  static constexpr int A = (L + 2 + 3) / 4 * 4;
-  static constexpr int B = (L + 2 + 3) / 4 * 4;
+  static constexpr int A = (L + 3 + 3) / 4 * 4;
+  static constexpr int B = (L + 1 + 3) / 4 * 4;
   static constexpr int W0 = A + B;
   static constexpr int W = ((W0 / 4) % 2 == 1) ? W0 : W0 + 4;   // odd # of 16B -> no conflicts
-  static constexpr int QU = 0, INFO = L, EU = L + 1;
-  static constexpr int Q0 = A, M = A + 1, ET = A + 1 + L;
+  static constexpr int QU = 0, Y0 = L, INFO = L + 1, EU = L + 2;
+  static constexpr int M = A, ET = A + L;
 };
 
 // Read at every mpsp_csr_create (tests lower it to route all rows through
@@ -117,7 +118,15 @@ __device__ __forceinline__ void load_entry(const PartView& P, const XView& x, in
   E.sx = __ldg(x.signs + col);
 }
 
-// Producer: t = RN(a*x), then its slot against the tag (ek, sk).
+// Producer: t = RN(a*x), then its slot against the tag (ek, sk): the
+// magnitude is aligned to E_used = ek - MARGIN (so the consumer only ever
+// shifts RIGHT by delta = E_s - E_used in [0, 31]: E_s may drop by up to
+// MARGIN or grow by up to 31 - MARGIN since the tag was read), the guard
+// limb stays in magnitude form, the L upper limbs are complemented when the
+// signs differ (Q_up = ~Y_up; the +1 of the two's complement is folded into
+// the consumer's carry-in).
+constexpr int MARGIN = 2;
+
 template <int L>
 __device__ __forceinline__ void produce_slot(uint32_t* slot, const Entry<L>& E, bool valid,
                                              int32_t ek, uint32_t sk) {
@@ -130,37 +139,22 @@ __device__ __forceinline__ void produce_slot(uint32_t* slot, const Entry<L>& E, 
   Y[0] = 0u;
 #pragma unroll
   for (int i = 0; i < L; ++i) Y[i + 1] = t.m[i];
-  int64_t d = (int64_t)ek - (int64_t)t.e;
-  int32_t eu;
-  uint32_t su;
-  if (ek == E_UNKNOWN || d < 0) {          // exact form w.r.t. its own exponent
-    d = 0;
-    eu = t.e;
-    su = t.s;
-  } else {
-    if (d > 32 * (L + 1)) d = 32 * (L + 1);
-    eu = ek;
-    su = sk;
-  }
+  int64_t d = (int64_t)ek - MARGIN - (int64_t)t.e;    // shift used (>= 1 for the fast path)
+  const bool rare = (ek == E_UNKNOWN) || d < 1;
+  if (rare) d = 0;
+  if (d > 32 * (L + 1)) d = 32 * (L + 1);
   uint32_t stk = 0u;
   shr_bits_sticky<L + 1>(Y, (uint32_t)d, stk);
   stk = stk ? 1u : 0u;
-  const uint32_t opp = t.s ^ su;
-  const uint32_t mask = 0u - opp;
-  const uint32_t c0 = opp & ((Y[0] == 0u) ? 1u : 0u) & (stk ^ 1u);
-  const uint32_t q0 = (Y[0] ^ mask) + (opp & (stk ^ 1u));
-  const uint32_t rb = q0 >> 31;
-  const uint32_t st = (q0 << 1) | stk;
-  const uint32_t inc = rb & (st != 0u ? 1u : 0u);
-  const uint32_t tie = rb & (st == 0u ? 1u : 0u);
-  uint32_t info = c0 | (inc << 1) | (tie << 2) | (opp << 4) | (stk << 5) | (t.s << 6) | (su << 7) |
-                  (d == 0 ? I_RARE : 0u);
+  const uint32_t su = rare ? t.s : sk;
+  const uint32_t mask = 0u - (t.s ^ su);
+  uint32_t info = (stk << 5) | (t.s << 6) | (su << 7) | (rare ? I_RARE : 0u);
   if (zero) info = I_ZERO;
+  slot[SL::Y0] = zero ? 0u : Y[0];
 #pragma unroll
   for (int i = 0; i < L; ++i) slot[SL::QU + i] = zero ? 0u : (Y[i + 1] ^ mask);
   slot[SL::INFO] = info;
-  slot[SL::EU] = (uint32_t)eu;
-  slot[SL::Q0] = q0;
+  slot[SL::EU] = (uint32_t)(rare ? t.e : ek - MARGIN);
 #pragma unroll
   for (int i = 0; i < L; ++i) slot[SL::M + i] = t.m[i];
   slot[SL::ET] = (uint32_t)t.e;
@@ -170,80 +164,16 @@ template <int L>
 struct ProdPrefetch { static constexpr bool on = (L <= 8); };
 
 // Consumer rare path: exact handling of one step from the exact accumulator
-// S (value before the step) and the slot.
+// S (value before the step): general add of the raw product in the slot.
 template <int L>
-__device__ __forceinline__ void exact_step(MP<L>& S, const uint32_t* sl, const uint32_t* qu,
-                                           uint32_t info, int32_t eu) {
+__device__ __forceinline__ void exact_step(MP<L>& S, const uint32_t* sl, uint32_t info) {
   using SL = LongSlot<L>;
   if (info & I_ZERO) return;
-  const uint32_t st_sign = (info >> 6) & 1u;
-  if (S.is_zero()) {
-#pragma unroll
-    for (int i = 0; i < L; ++i) S.m[i] = sl[SL::M + i];
-    S.e = (int32_t)sl[SL::ET];
-    S.s = st_sign;
-    return;
-  }
-  // recover the aligned magnitude Y (L+1 limbs) and the sticky flag
-  const uint32_t stk0 = (info >> 5) & 1u;
-  uint32_t Y[L + 1];
-  Y[0] = sl[SL::Q0];
-#pragma unroll
-  for (int i = 0; i < L; ++i) Y[i + 1] = qu[i];
-  if (info & I_OPP) {
-    // stored: q0 = ~Y0 + 1 - stk (mod 2^32), Q_up = ~Y_up (the carry c0 of
-    // the full complement travels separately in cin)
-    Y[0] = 0u - Y[0] - stk0;
-#pragma unroll
-    for (int i = 1; i <= L; ++i) Y[i] = ~Y[i];
-  }
-  uint32_t stk = stk0;
-  bool general = false;
-  const int64_t delta = (int64_t)S.e - (int64_t)eu;
-  if (delta > 0 && delta <= 31) {
-    const uint32_t r = (uint32_t)delta;
-    stk |= (Y[0] << (32u - r)) != 0u ? 1u : 0u;
-#pragma unroll
-    for (int i = 0; i < L; ++i) Y[i] = __funnelshift_r(Y[i], Y[i + 1], r);
-    Y[L] >>= r;
-  } else if (delta < 0 && delta >= -31 && __clz(Y[L]) >= (int)(-delta)) {
-    const uint32_t r = (uint32_t)(-delta);
-#pragma unroll
-    for (int i = L; i > 0; --i) Y[i] = __funnelshift_l(Y[i - 1], Y[i], r);
-    Y[0] <<= r;
-  } else if (delta != 0) {
-    general = true;
-  }
-  if (!general) {
-    const uint32_t opp = st_sign ^ S.s;
-    const uint32_t mask = 0u - opp;
-    const uint32_t c0 = opp & ((Y[0] == 0u) ? 1u : 0u) & (stk ^ 1u);
-    const uint32_t q0 = (Y[0] ^ mask) + (opp & (stk ^ 1u));
-    uint32_t Q[L];
-#pragma unroll
-    for (int i = 0; i < L; ++i) Q[i] = Y[i + 1] ^ mask;
-    const uint32_t rb = q0 >> 31;
-    const uint32_t st = (q0 << 1) | stk;
-    const uint32_t lsb = (S.m[0] ^ Q[0] ^ c0) & 1u;
-    const uint32_t inc = rb & ((st != 0u) | lsb);
-    uint32_t R[L];
-    uint32_t co = add_n<L>(R, S.m, Q);
-    co += inc_n<L>(R, c0);
-    co += inc_n<L>(R, inc);
-    const bool bad = opp ? ((co == 0u) || (R[L - 1] < 0x80000000u) ||
-                            (R[L - 1] == 0x80000000u && inc))
-                         : (co != 0u);
-    if (!bad) {
-#pragma unroll
-      for (int i = 0; i < L; ++i) S.m[i] = R[i];
-      return;
-    }
-  }
-  MP<L> t;                                  // general add of the raw product
+  MP<L> t;
 #pragma unroll
   for (int i = 0; i < L; ++i) t.m[i] = sl[SL::M + i];
   t.e = (int32_t)sl[SL::ET];
-  t.s = st_sign;
+  t.s = (info >> 6) & 1u;
   mp_add<L>(S, t);
 }
 
@@ -359,25 +289,45 @@ __global__ void __launch_bounds__(LTHREADS) spmv_long(PartView P, XView x, YView
         }
         const uint32_t info = Aw[SL::INFO];
         const int32_t eu = (int32_t)Aw[SL::EU];
-        // ---- fast step, branch-free: carry-save S += Q_up + cin
-        const uint32_t c0 = info & I_C0;
-        const uint32_t lsb = (Acs[0] ^ Aw[SL::QU] ^ c0) & 1u;
-        const uint32_t cin = c0 + ((info >> 1) & 1u) + (((info >> 2) & 1u) & lsb);
+        // ---- fast step, branch-free
+        // realign right by r = E_s - E_used in [0, 31] (stale tags included)
+        const int32_t delta = Ecur - eu;
+        const bool ok_shift = (delta >= 0) && (delta <= 31);
+        const uint32_t r = ok_shift ? (uint32_t)delta : 0u;
+        const uint32_t stk0 = (info >> 5) & 1u;
+        const uint32_t opp = ((info >> 6) ^ (info >> 7)) & 1u;   // sign_t != sign used
+        const uint32_t mask = 0u - opp;
+        const uint32_t y1 = Aw[SL::QU] ^ mask;
+        const uint32_t y0 = __funnelshift_r(Aw[SL::Y0], y1, r);
+        const uint32_t stk = stk0 | ((r != 0u && (Aw[SL::Y0] << (32u - r)) != 0u) ? 1u : 0u);
+        uint32_t Q[L];
+#pragma unroll
+        for (int i = 0; i < L - 1; ++i) Q[i] = __funnelshift_r(Aw[SL::QU + i], Aw[SL::QU + i + 1], r);
+        Q[L - 1] = __funnelshift_r(Aw[SL::QU + L - 1], mask, r);   // sign-fill when complemented
+        // RNE decision of the step in S's binade (guard limb of S is zero)
+        const uint32_t nstk = stk ^ 1u;
+        const uint32_t c0 = opp & ((y0 == 0u) ? 1u : 0u) & nstk;
+        const uint32_t q0 = (y0 ^ mask) + (opp & nstk);
+        const uint32_t rb = q0 >> 31;
+        const uint32_t stn = ((q0 << 1) | stk) != 0u ? 1u : 0u;
+        const uint32_t lsb = (Acs[0] ^ Q[0] ^ c0) & 1u;
+        const uint32_t cin = c0 + (rb & (stn | lsb));          // 0..2
+        // carry-save S += Q + cin (carries out of the top limb dropped)
         uint32_t A1[L], C1[L];
         C1[0] = 0u;
         {
-          const uint64_t t0 = (uint64_t)Acs[0] + Aw[SL::QU] + cin;
+          const uint64_t t0 = (uint64_t)Acs[0] + Q[0] + cin;
           A1[0] = (uint32_t)t0;
           if (L > 1) C1[1] = (uint32_t)(t0 >> 32);
 #pragma unroll
           for (int i = 1; i < L; ++i) {
-            const uint64_t ti = (uint64_t)Acs[i] + Aw[SL::QU + i] + Ccs[i];
+            const uint64_t ti = (uint64_t)Acs[i] + Q[i] + Ccs[i];
             A1[i] = (uint32_t)ti;
-            if (i + 1 < L) C1[i + 1] = (uint32_t)(ti >> 32);   // top carry dropped (mod 2^(32L))
+            if (i + 1 < L) C1[i + 1] = (uint32_t)(ti >> 32);
           }
         }
         const uint64_t T = (uint64_t)A1[L - 1] + (L > 1 ? C1[L - 1] : 0u);
-        const bool tag_ok = (eu == Ecur) && (((info >> 7) & 1u) == Scur) && !(info & I_RARE);
+        const bool tag_ok = ok_shift && (((info >> 7) & 1u) == Scur) && !(info & I_RARE);
         const bool safe = (T >= 0x80000001ull) && (T <= 0xFFFFFFFEull);
         const bool zslot = (info & I_ZERO) != 0u;
         const bool need = cons && (szero ? !zslot : !(safe && (zslot || tag_ok)));
@@ -392,10 +342,7 @@ __global__ void __launch_bounds__(LTHREADS) spmv_long(PartView P, XView x, YView
             } else {
               uint32_t R[L];
               add_n<L>(R, Acs, Ccs);                 // resolve carries (mod 2^(32L))
-              uint32_t Qh[L];
-#pragma unroll
-              for (int i = 0; i < L; ++i) Qh[i] = Aw[SL::QU + i];
-              sub_n<L>(R, R, Qh, 0u);
+              sub_n<L>(R, R, Q, 0u);
               uint32_t cv[L];
               cv[0] = cin;
 #pragma unroll
@@ -406,10 +353,7 @@ __global__ void __launch_bounds__(LTHREADS) spmv_long(PartView P, XView x, YView
               S.e = Ecur;
               S.s = Scur;
             }
-            uint32_t qu[L];
-#pragma unroll
-            for (int i = 0; i < L; ++i) qu[i] = Aw[SL::QU + i];
-            exact_step<L>(S, sl, qu, info, eu);
+            exact_step<L>(S, sl, info);
 #pragma unroll
             for (int i = 0; i < L; ++i) { Acs[i] = S.m[i]; Ccs[i] = 0u; }
             szero = S.is_zero();
@@ -447,7 +391,7 @@ __global__ void __launch_bounds__(LTHREADS) spmv_long(PartView P, XView x, YView
             g_long_chk[3] = Aw[SL::INFO]; g_long_chk[4] = (uint32_t)Aw[SL::EU];
             g_long_chk[5] = (uint32_t)dbg_E0; g_long_chk[6] = dbg_S0; g_long_chk[7] = dbg_z0;
             g_long_chk[8] = (uint32_t)Ecur; g_long_chk[9] = Scur; g_long_chk[10] = (uint32_t)Sref.e;
-            g_long_chk[11] = Sref.s; g_long_chk[12] = sl[SL::Q0]; g_long_chk[13] = (uint32_t)sl[SL::ET];
+            g_long_chk[11] = Sref.s; g_long_chk[12] = Aw[SL::Y0]; g_long_chk[13] = (uint32_t)sl[SL::ET];
             for (int i = 0; i < L && i < 8; ++i) {
               g_long_chk[16 + i] = Sc.m[i]; g_long_chk[24 + i] = Sref.m[i];
               g_long_chk[32 + i] = Aw[SL::QU + i]; g_long_chk[40 + i] = sl[SL::M + i];
