@@ -52,7 +52,7 @@ constexpr int32_t E_UNKNOWN = INT_MIN;
 #ifdef MPSP_LONG_PROFILE
 // debug build only: per-chunk timestamps of CTA 0 (producer role 1 lane 0,
 // consumer lane 0): [chunk][0..3] = prod start, prod end, cons start, cons end
-__device__ long long g_long_prof[4096][4];
+__device__ long long g_long_prof[4096][6];
 #define LPROF(c, k) do { if (blockIdx.x == 0 && (c) < 4096) g_long_prof[c][k] = clock64(); } while (0)
 #else
 #define LPROF(c, k) do { } while (0)
@@ -177,6 +177,82 @@ __device__ __forceinline__ void exact_step(MP<L>& S, const uint32_t* sl, uint32_
   mp_add<L>(S, t);
 }
 
+// One consumer step's branch-free arithmetic for this lane's K limbs of its
+// row (LPR lanes per row): realign the slot by E_s - E_used, RNE decision,
+// carry-save add with the bottom pending carry (ck > 0) or the carry-in
+// (ck == 0).  BLOCK: the margin check assumes up to CG undelivered carries.
+constexpr int CG = 4;                       // fast steps per block
+
+template <int K>
+struct StepOut {
+  uint32_t A1[K], C1[K], Q[K];
+  uint32_t co, cin, info;
+  bool need, zslot, tag_ok;
+};
+
+template <int L, int LPR, int K, bool BLOCK>
+__device__ __forceinline__ void cons_compute(const uint32_t* sl, int ck, const uint32_t (&Acs)[K],
+                                             const uint32_t (&Ccs)[K], int32_t Ecur, uint32_t Scur,
+                                             StepOut<K>& o) {
+  using SL = LongSlot<L>;
+  const uint32_t info = sl[SL::INFO];
+  const int32_t eu = (int32_t)sl[SL::EU];
+  const uint32_t Y0 = sl[SL::Y0];
+  const uint32_t qw0 = sl[SL::QU];
+  const uint32_t opp = ((info >> 6) ^ (info >> 7)) & 1u;     // sign_t != sign used
+  const uint32_t mask = 0u - opp;
+  uint32_t Qm[K + 1];
+#pragma unroll
+  for (int i = 0; i <= K; ++i) {
+    const int idx = ck * K + i;
+    const uint32_t v = sl[SL::QU + (idx < L ? idx : L - 1)];
+    Qm[i] = idx < L ? v : mask;                      // sign fill above the top limb
+  }
+  const int32_t delta = Ecur - eu;
+  const bool ok_shift = (delta >= 0) && (delta <= 31);
+  const uint32_t r = ok_shift ? (uint32_t)delta : 0u;
+  const uint32_t stk0 = (info >> 5) & 1u;
+  const uint32_t y1 = qw0 ^ mask;
+  const uint32_t y0 = __funnelshift_r(Y0, y1, r);
+  const uint32_t stk = stk0 | ((r != 0u && (Y0 << (32u - r)) != 0u) ? 1u : 0u);
+#pragma unroll
+  for (int i = 0; i < K; ++i) o.Q[i] = __funnelshift_r(Qm[i], Qm[i + 1], r);
+  const uint32_t nstk = stk ^ 1u;
+  const uint32_t c0 = opp & ((y0 == 0u) ? 1u : 0u) & nstk;
+  const uint32_t q0 = (y0 ^ mask) + (opp & nstk);
+  const uint32_t rb = q0 >> 31;
+  const uint32_t stn = ((q0 << 1) | stk) != 0u ? 1u : 0u;
+  const uint32_t lsb = (Acs[0] ^ o.Q[0] ^ c0) & 1u;
+  o.cin = c0 + (rb & (stn | lsb));                  // 0..2 (meaningful at ck 0)
+  {
+    const uint64_t t0 = (uint64_t)Acs[0] + o.Q[0] + (ck == 0 ? o.cin : Ccs[0]);
+    o.A1[0] = (uint32_t)t0;
+    uint32_t co = (uint32_t)(t0 >> 32);
+#pragma unroll
+    for (int i = 1; i < K; ++i) {
+      o.C1[i] = co;
+      const uint64_t ti = (uint64_t)Acs[i] + o.Q[i] + Ccs[i];
+      o.A1[i] = (uint32_t)ti;
+      co = (uint32_t)(ti >> 32);
+    }
+    o.co = co;
+    o.C1[0] = 0u;
+  }
+  o.info = info;
+  o.zslot = (info & I_ZERO) != 0u;
+  o.tag_ok = ok_shift && (((info >> 7) & 1u) == Scur) && !(info & I_RARE);
+  if (BLOCK) {
+    // top lane: true top in [T, T + 1 + undelivered carries] (the latter only
+    // reach the top limb directly when K == 1)
+    const uint64_t T = (uint64_t)o.A1[K - 1] + (K > 1 ? o.C1[K - 1] : 0u);
+    const uint64_t hi = (K == 1) ? 0xFFFFFFFEull - CG : 0xFFFFFFFEull;
+    const bool safe = (ck != LPR - 1) || ((T >= 0x80000001ull) && (T <= hi));
+    o.need = !(safe && (o.zslot || o.tag_ok));
+  } else {
+    o.need = false;                                  // careful mode checks after delivery
+  }
+}
+
 template <int L>
 __global__ void __launch_bounds__(LTHREADS) spmv_long(PartView P, XView x, YView y) {
   extern __shared__ uint32_t smem[];
@@ -199,12 +275,18 @@ __global__ void __launch_bounds__(LTHREADS) spmv_long(PartView P, XView x, YView
   __syncthreads();
   const int nchunks = (width + LC - 1) / LC;
 
-  // ---- consumer state (role 0, lanes < LR): S in carry-save form
-  const bool cons = (warp == 0 && lane < LR);
-  uint32_t Acs[L], Ccs[L];                 // limbs and pending carries (Ccs[0] unused)
+  // ---- consumer (role 0): LPR lanes per row, K limbs per lane; each row's
+  // accumulator S in carry-save form spread over its lanes
+  constexpr int LPR = L < 4 ? L : 4;
+  constexpr int K = L / LPR;
+  const int crow = lane / LPR;                       // row of this lane (>= LR: idle)
+  const int ck = lane % LPR;                         // limb group: limbs [ck*K, ck*K+K)
+  const bool cons = (warp == 0 && crow < LR);
+  const int crw = crow < LR ? crow : 0;              // idle lanes mirror row 0, never commit
+  uint32_t Acs[K], Ccs[K];                           // limbs, pending carries into them
 #pragma unroll
-  for (int i = 0; i < L; ++i) { Acs[i] = 0u; Ccs[i] = 0u; }
-  int32_t Ecur = E_UNKNOWN;
+  for (int i = 0; i < K; ++i) { Acs[i] = 0u; Ccs[i] = 0u; }
+  int32_t Ecur = E_UNKNOWN;                          // replicated over the row's lanes
   uint32_t Scur = 0u;
   bool szero = true;
 #ifdef MPSP_LONG_CHECK
@@ -269,151 +351,185 @@ __global__ void __launch_bounds__(LTHREADS) spmv_long(PartView P, XView x, YView
       if (lane == 0) LPROF(cc, 2);
       const uint32_t* B = buf + (cc & 1) * (LC * LR * SW);
       const int jn = min(LC, width - cc * LC);
-      constexpr int NV = SL::A / 4;                       // 128-bit words of part A
-      const int ln = lane < LR ? lane : 0;                // idle lanes mirror lane 0
-      for (int jj = 0; jj < jn; ++jj) {
-        const uint32_t* sl = B + (jj * LR + ln) * SW;
-#ifdef MPSP_LONG_CHECK
-        const int32_t dbg_E0 = Ecur;
-        const uint32_t dbg_S0 = Scur;
-        const bool dbg_z0 = szero;
+      // careful per-step mode (per-step carry delivery and checks, exact
+      // rare path) for the rows in `rrow`, steps [jb, jb+gn)
+      auto careful = [&](int jb, int gn, bool rrow) {
+        for (int u = 0; u < gn; ++u) {
+          const uint32_t* sl = B + ((jb + u) * LR + crw) * SW;
+          StepOut<K> o;
+          cons_compute<L, LPR, K, false>(sl, ck, Acs, Ccs, Ecur, Scur, o);
+          uint32_t cup = __shfl_up_sync(0xffffffffu, o.co, 1);
+          if (ck == 0) cup = 0u;
+          o.C1[0] = cup;
+          const uint64_t T = (uint64_t)o.A1[K - 1] + o.C1[K - 1];
+          const bool safe = (ck != LPR - 1) || ((T >= 0x80000001ull) && (T <= 0xFFFFFFFEull));
+          const bool need_lane = rrow && (szero ? !o.zslot : !(safe && (o.zslot || o.tag_ok)));
+          if (rrow) {
+#pragma unroll
+            for (int i = 0; i < K; ++i) { Acs[i] = o.A1[i]; Ccs[i] = o.C1[i]; }
+          }
+          const unsigned bal2 = __ballot_sync(0xffffffffu, need_lane);
+          if (bal2 != 0u) {
+            const bool need_row = rrow && ((bal2 >> (crow * LPR)) & ((1u << LPR) - 1u)) != 0u;
+            uint32_t Af[L], Cf[L], Qf[L];
+#pragma unroll
+            for (int i = 0; i < L; ++i) {
+              const int src = crw * LPR + i / K;
+              Af[i] = __shfl_sync(0xffffffffu, Acs[i % K], src);
+              Cf[i] = __shfl_sync(0xffffffffu, Ccs[i % K], src);
+              Qf[i] = __shfl_sync(0xffffffffu, o.Q[i % K], src);
+            }
+            const uint32_t cin_row = __shfl_sync(0xffffffffu, o.cin, crw * LPR);
+            if (need_row) {
+              MP<L> S;
+              if (szero) {
+                S.set_zero();
+              } else {
+                add_n<L>(S.m, Af, Cf);               // resolve carries (mod 2^(32L))
+                sub_n<L>(S.m, S.m, Qf, 0u);
+                uint32_t cv[L];
+                cv[0] = cin_row;
+#pragma unroll
+                for (int i = 1; i < L; ++i) cv[i] = 0u;
+                sub_n<L>(S.m, S.m, cv, 0u);
+                S.e = Ecur;
+                S.s = Scur;
+              }
+              exact_step<L>(S, sl, o.info);
+#pragma unroll
+              for (int i = 0; i < K; ++i) {
+                uint32_t v = S.m[i];
+#pragma unroll
+                for (int g = 1; g < LPR; ++g) v = (ck == g) ? S.m[g * K + i] : v;
+                Acs[i] = v;
+                Ccs[i] = 0u;
+              }
+              szero = S.is_zero();
+              const int32_t Enew = szero ? E_UNKNOWN : S.e;
+              const uint32_t Snew = szero ? 0u : S.s;
+              if (ck == 0 && (Enew != Ecur || Snew != Scur))
+                key_pub[crow] = ((unsigned long long)Snew << 32) | (uint32_t)Enew;
+              Ecur = Enew;
+              Scur = Snew;
+            }
+          }
+        }
+      };
+      const int nfull = jn / CG;
+      for (int b = 0; b < nfull; ++b) {
+        const int jb = b * CG;
+        // ---- block of CG fast steps, straight-line code: no branch, vote or
+        // shuffle inside; cross-lane carries are counted, delivered at the end
+        uint32_t As0[K], Cs0[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) { As0[i] = Acs[i]; Cs0[i] = Ccs[i]; }
+        bool nacc = false;
+        uint32_t cacc = 0u;
+#pragma unroll
+        for (int u = 0; u < CG; ++u) {
+          const uint32_t* sl = B + ((jb + u) * LR + crw) * SW;
+          StepOut<K> o;
+          cons_compute<L, LPR, K, true>(sl, ck, Acs, Ccs, Ecur, Scur, o);
+#ifdef MPSP_LONG_PROFILE
+          if (blockIdx.x == 0 && cons && ck == 0 && cc < 4096 && !o.zslot) {
+            const int32_t dl = Ecur - (int32_t)sl[SL::EU];
+            atomicAdd((unsigned long long*)&g_long_prof[cc][5], (unsigned long long)(dl != MARGIN) << 20);
+          }
 #endif
-        uint32_t Aw[NV * 4];
+#pragma unroll
+          for (int i = 0; i < K; ++i) { Acs[i] = o.A1[i]; Ccs[i] = o.C1[i]; }
+          Ccs[0] = 0u;                                     // bottom pending consumed
+          cacc += o.co;
+          nacc = nacc || (cons && (szero ? !o.zslot : o.need));
+        }
         {
-          const uint4* v = reinterpret_cast<const uint4*>(sl);
-#pragma unroll
-          for (int q = 0; q < NV; ++q) {
-            const uint4 u4 = v[q];
-            Aw[4 * q] = u4.x; Aw[4 * q + 1] = u4.y; Aw[4 * q + 2] = u4.z; Aw[4 * q + 3] = u4.w;
-          }
+          uint32_t cup = __shfl_up_sync(0xffffffffu, cacc, 1);
+          if (ck == 0) cup = 0u;
+          Ccs[0] += cup;
         }
-        const uint32_t info = Aw[SL::INFO];
-        const int32_t eu = (int32_t)Aw[SL::EU];
-        // ---- fast step, branch-free
-        // realign right by r = E_s - E_used in [0, 31] (stale tags included)
-        const int32_t delta = Ecur - eu;
-        const bool ok_shift = (delta >= 0) && (delta <= 31);
-        const uint32_t r = ok_shift ? (uint32_t)delta : 0u;
-        const uint32_t stk0 = (info >> 5) & 1u;
-        const uint32_t opp = ((info >> 6) ^ (info >> 7)) & 1u;   // sign_t != sign used
-        const uint32_t mask = 0u - opp;
-        const uint32_t y1 = Aw[SL::QU] ^ mask;
-        const uint32_t y0 = __funnelshift_r(Aw[SL::Y0], y1, r);
-        const uint32_t stk = stk0 | ((r != 0u && (Aw[SL::Y0] << (32u - r)) != 0u) ? 1u : 0u);
-        uint32_t Q[L];
-#pragma unroll
-        for (int i = 0; i < L - 1; ++i) Q[i] = __funnelshift_r(Aw[SL::QU + i], Aw[SL::QU + i + 1], r);
-        Q[L - 1] = __funnelshift_r(Aw[SL::QU + L - 1], mask, r);   // sign-fill when complemented
-        // RNE decision of the step in S's binade (guard limb of S is zero)
-        const uint32_t nstk = stk ^ 1u;
-        const uint32_t c0 = opp & ((y0 == 0u) ? 1u : 0u) & nstk;
-        const uint32_t q0 = (y0 ^ mask) + (opp & nstk);
-        const uint32_t rb = q0 >> 31;
-        const uint32_t stn = ((q0 << 1) | stk) != 0u ? 1u : 0u;
-        const uint32_t lsb = (Acs[0] ^ Q[0] ^ c0) & 1u;
-        const uint32_t cin = c0 + (rb & (stn | lsb));          // 0..2
-        // carry-save S += Q + cin (carries out of the top limb dropped)
-        uint32_t A1[L], C1[L];
-        C1[0] = 0u;
-        {
-          const uint64_t t0 = (uint64_t)Acs[0] + Q[0] + cin;
-          A1[0] = (uint32_t)t0;
-          if (L > 1) C1[1] = (uint32_t)(t0 >> 32);
-#pragma unroll
-          for (int i = 1; i < L; ++i) {
-            const uint64_t ti = (uint64_t)Acs[i] + Q[i] + Ccs[i];
-            A1[i] = (uint32_t)ti;
-            if (i + 1 < L) C1[i + 1] = (uint32_t)(ti >> 32);
-          }
-        }
-        const uint64_t T = (uint64_t)A1[L - 1] + (L > 1 ? C1[L - 1] : 0u);
-        const bool tag_ok = ok_shift && (((info >> 7) & 1u) == Scur) && !(info & I_RARE);
-        const bool safe = (T >= 0x80000001ull) && (T <= 0xFFFFFFFEull);
-        const bool zslot = (info & I_ZERO) != 0u;
-        const bool need = cons && (szero ? !zslot : !(safe && (zslot || tag_ok)));
-#pragma unroll
-        for (int i = 0; i < L; ++i) { Acs[i] = A1[i]; Ccs[i] = C1[i]; }
-        if (__any_sync(0xffffffffu, need)) {
-          if (need) {
-            // ---- rare path: restore the exact S before this step, redo exactly
-            MP<L> S;
-            if (szero) {
-              S.set_zero();
-            } else {
-              uint32_t R[L];
-              add_n<L>(R, Acs, Ccs);                 // resolve carries (mod 2^(32L))
-              sub_n<L>(R, R, Q, 0u);
-              uint32_t cv[L];
-              cv[0] = cin;
-#pragma unroll
-              for (int i = 1; i < L; ++i) cv[i] = 0u;
-              sub_n<L>(R, R, cv, 0u);
-#pragma unroll
-              for (int i = 0; i < L; ++i) S.m[i] = R[i];
-              S.e = Ecur;
-              S.s = Scur;
-            }
-            exact_step<L>(S, sl, info);
-#pragma unroll
-            for (int i = 0; i < L; ++i) { Acs[i] = S.m[i]; Ccs[i] = 0u; }
-            szero = S.is_zero();
-            const int32_t Enew = szero ? E_UNKNOWN : S.e;
-            const uint32_t Snew = szero ? 0u : S.s;
-            if (Enew != Ecur || Snew != Scur)
-              key_pub[lane] = ((unsigned long long)Snew << 32) | (uint32_t)Enew;
-            Ecur = Enew;
-            Scur = Snew;
-          }
-        }
-#ifdef MPSP_LONG_CHECK
-        if (cons) {
-          {
-            const uint32_t inf = Aw[SL::INFO];
-            if (!(inf & I_ZERO)) {
-              MP<L> t;
-#pragma unroll
-              for (int i = 0; i < L; ++i) t.m[i] = sl[SL::M + i];
-              t.e = (int32_t)sl[SL::ET];
-              t.s = (inf >> 6) & 1u;
-              mp_add<L>(Sref, t);
-            }
-          }
-          MP<L> Sc;
-          add_n<L>(Sc.m, Acs, Ccs);
-          if (szero) Sc.set_zero();
-          bool diff = (Sc.is_zero() != Sref.is_zero());
-          if (!Sref.is_zero()) {
-            for (int i = 0; i < L; ++i) diff |= Sc.m[i] != Sref.m[i];
-            diff |= (Ecur != Sref.e) || (Scur != Sref.s);
-          }
-          if (diff && atomicExch(&g_long_chk_flag, 1) == 0) {
-            g_long_chk[0] = blockIdx.x; g_long_chk[1] = lane; g_long_chk[2] = cc * LC + jj;
-            g_long_chk[3] = Aw[SL::INFO]; g_long_chk[4] = (uint32_t)Aw[SL::EU];
-            g_long_chk[5] = (uint32_t)dbg_E0; g_long_chk[6] = dbg_S0; g_long_chk[7] = dbg_z0;
-            g_long_chk[8] = (uint32_t)Ecur; g_long_chk[9] = Scur; g_long_chk[10] = (uint32_t)Sref.e;
-            g_long_chk[11] = Sref.s; g_long_chk[12] = Aw[SL::Y0]; g_long_chk[13] = (uint32_t)sl[SL::ET];
-            for (int i = 0; i < L && i < 8; ++i) {
-              g_long_chk[16 + i] = Sc.m[i]; g_long_chk[24 + i] = Sref.m[i];
-              g_long_chk[32 + i] = Aw[SL::QU + i]; g_long_chk[40 + i] = sl[SL::M + i];
-            }
-          }
-          // continue from the reference to keep later checks meaningful
+        const unsigned bal = __ballot_sync(0xffffffffu, nacc);
+#ifdef MPSP_LONG_PROFILE
+        if (blockIdx.x == 0 && lane == 0 && cc < 4096) {
+          g_long_prof[cc][4] += (bal != 0u);
+          g_long_prof[cc][5] += __popc(bal);
         }
 #endif
+        if (bal != 0u) {
+          const bool rrow = cons && ((bal >> (crow * LPR)) & ((1u << LPR) - 1u)) != 0u;
+          if (rrow) {
+#pragma unroll
+            for (int i = 0; i < K; ++i) { Acs[i] = As0[i]; Ccs[i] = Cs0[i]; }
+          }
+          careful(jb, CG, rrow);
+        }
+      }
+      if (nfull * CG < jn) careful(nfull * CG, jn - nfull * CG, cons);
+      {
+        const int jb = 0, gn = jn;
+#ifdef MPSP_LONG_CHECK
+        for (int u = 0; u < gn; ++u) {
+          const uint32_t* sl = B + ((jb + u) * LR + crw) * SW;
+          const uint32_t info = sl[SL::INFO];
+          if (cons && ck == 0 && !(info & I_ZERO)) {
+            MP<L> t;
+#pragma unroll
+            for (int i = 0; i < L; ++i) t.m[i] = sl[SL::M + i];
+            t.e = (int32_t)sl[SL::ET];
+            t.s = (info >> 6) & 1u;
+            mp_add<L>(Sref, t);
+          }
+        }
+        {
+          uint32_t Af[L], Cf[L];
+#pragma unroll
+          for (int i = 0; i < L; ++i) {
+            const int src = crw * LPR + i / K;
+            Af[i] = __shfl_sync(0xffffffffu, Acs[i % K], src);
+            Cf[i] = __shfl_sync(0xffffffffu, Ccs[i % K], src);
+          }
+          if (cons && ck == 0) {
+            MP<L> Sc;
+            add_n<L>(Sc.m, Af, Cf);
+            if (szero) Sc.set_zero();
+            bool diff = (Sc.is_zero() != Sref.is_zero());
+            if (!Sref.is_zero()) {
+              for (int i = 0; i < L; ++i) diff |= Sc.m[i] != Sref.m[i];
+              diff |= (Ecur != Sref.e) || (Scur != Sref.s);
+            }
+            if (diff && atomicExch(&g_long_chk_flag, 1) == 0) {
+              g_long_chk[0] = blockIdx.x; g_long_chk[1] = crow; g_long_chk[2] = cc * LC + jb;
+              g_long_chk[8] = (uint32_t)Ecur; g_long_chk[9] = Scur; g_long_chk[10] = (uint32_t)Sref.e;
+              g_long_chk[11] = Sref.s;
+              for (int i = 0; i < L && i < 8; ++i) { g_long_chk[16 + i] = Sc.m[i]; g_long_chk[24 + i] = Sref.m[i]; }
+            }
+          }
+        }
+#endif
+        (void)jb;
+        (void)gn;
       }
       if (lane == 0) LPROF(cc, 3);
     }
     __syncthreads();
   }
-  if (cons) {
-    const int row = P.slot_row[slot0 + lane];
-    if (row >= 0) {
-      MP<L> S;
-      add_n<L>(S.m, Acs, Ccs);
-      if (szero) S.set_zero();
-      S.e = Ecur;
-      S.s = Scur;
-      store_y<L>(y, row, S);
+  if (warp == 0) {
+    uint32_t Af[L], Cf[L];
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      const int src = crw * LPR + i / K;
+      Af[i] = __shfl_sync(0xffffffffu, Acs[i % K], src);
+      Cf[i] = __shfl_sync(0xffffffffu, Ccs[i % K], src);
+    }
+    if (cons && ck == 0) {
+      const int row = P.slot_row[slot0 + crow];
+      if (row >= 0) {
+        MP<L> S;
+        add_n<L>(S.m, Af, Cf);
+        if (szero) S.set_zero();
+        S.e = Ecur;
+        S.s = Scur;
+        store_y<L>(y, row, S);
+      }
     }
   }
 }
@@ -457,6 +573,6 @@ extern "C" int mpsp_debug_long_check(unsigned long long* out) {
 #ifdef MPSP_LONG_PROFILE
 extern "C" int mpsp_debug_long_profile(long long* out, int nchunks) {
   if (nchunks > 4096) nchunks = 4096;
-  return (int)cudaMemcpyFromSymbol(out, mpsp::g_long_prof, (size_t)nchunks * 4 * sizeof(long long));
+  return (int)cudaMemcpyFromSymbol(out, mpsp::g_long_prof, (size_t)nchunks * 6 * sizeof(long long));
 }
 #endif

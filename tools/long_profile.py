@@ -27,13 +27,14 @@ for _ in range(2):
     A.spmv(x)
 torch.cuda.synchronize()
 n = 260
-buf = (ctypes.c_longlong * (n * 4))()
+buf = (ctypes.c_longlong * (n * 6))()
 lib.mpsp_debug_long_profile.argtypes = [ctypes.c_void_p, ctypes.c_int]
 print("rc", lib.mpsp_debug_long_profile(buf, n))
-t = np.array(buf[:], dtype=np.int64).reshape(n, 4)
+t = np.array(buf[:], dtype=np.int64).reshape(n, 6)
 t0 = t[0, 0]
 for c in list(range(0, 12)) + list(range(100, 106)) + list(range(200, 212)):
     if c < n and t[c, 0]:
-        print(c, (t[c] - t0).tolist(), "prod", t[c, 1] - t[c, 0], "cons", t[c, 3] - t[c, 2])
+        print(c, (t[c, :4] - t0).tolist(), "prod", t[c, 1] - t[c, 0], "cons", t[c, 3] - t[c, 2], "rare steps", t[c, 4], "rare lanes", t[c, 5] & 0xFFFFF, "stale row-steps", t[c, 5] >> 20)
 valid = t[:, 0] > 0
+print("total rare steps", t[:, 4].sum(), "of", int(valid.sum()) * 24, "stale row-steps", (t[:, 5] >> 20).sum(), "of", int(valid.sum()) * 24 * 8)
 print("avg prod", np.mean((t[:, 1] - t[:, 0])[valid]), "avg cons", np.mean((t[:, 3] - t[:, 2])[t[:, 2] > 0]))
