@@ -1,8 +1,13 @@
 // layout.h - device layout of one row block of A (or A^T), shared by the
 // host builder and the kernels.
 //
-// Rows are sorted by length (descending, stable) and cut into SELL slices of
-// 32 rows; slice s holds w_s = (longest row in the slice) positions.  Entry
+// Rows are sorted by length (descending, stable).  The rows longer than the
+// long-row threshold come first as WARP ROWS (one warp per row, spmv_wrow):
+// warp row i owns entries [wrow_ptr[i], wrow_ptr[i] + len rounded up to 32),
+// entry j of the row at E = wrow_ptr[i] + j, i.e. group g = E/32 and lane
+// l = j % 32 in the limb formula below, so a warp's 32 consecutive entries
+// load as coalesced 512 B chunks.  The remaining rows are cut into SELL
+// slices of 32 rows; slice s holds w_s = (longest row in the slice) positions.  Entry
 // (slice s, position j, lane l) has entry index E = slice_ptr[s] + 32*j + l,
 // i.e. it lives in "group" g = E/32 = slice_ptr[s]/32 + j.
 //   col[E], expw[E]   : int32 column index and packed exponent word
@@ -27,11 +32,13 @@ struct PartView {
   const int32_t* col;         // [nentries]
   const int32_t* expw;        // [nentries]
   const uint32_t* limbs;      // [nentries * L]
-  int64_t nslots;             // 32 * nslices
+  int64_t nslots;             // 32 * nslices (SELL part: short rows)
   int64_t nslices;
-  int64_t nlong;              // slices [0, nlong) hold rows longer than the
-                              // long-row threshold (spmv_long); the rest
-                              // go to spmv_sell
+  // warp rows (rows longer than the long-row threshold), longest first
+  int64_t nwrow;
+  const int64_t* wrow_ptr;    // [nwrow] first entry (multiple of 32)
+  const int32_t* wrow_row;    // [nwrow] output row (local)
+  const int32_t* wrow_len;    // [nwrow]
 };
 
 struct XView {
@@ -48,9 +55,9 @@ struct YView {
 
 // Launch the SpMV over one part on `stream`; returns a cudaError_t value.
 int launch_spmv(int L, const PartView& P, const XView& x, const YView& y, void* stream);
-// Long-row kernel over slices [0, P.nlong); returns a cudaError_t value.
+// Warp-row kernel over the P.nwrow long rows; returns a cudaError_t value.
 int launch_spmv_long(int L, const PartView& P, const XView& x, const YView& y, void* stream);
-// Row-length threshold above which a slice goes to the long-row kernel.
+// Row-length threshold above which a row goes to the warp-row kernel.
 int long_row_threshold();
 // Launch counter increment (shared by the kernel files).
 void launch_counter_add(int64_t k);

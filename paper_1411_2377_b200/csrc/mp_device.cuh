@@ -102,6 +102,23 @@ __device__ __forceinline__ uint32_t rne_increment(uint32_t (&m)[L], uint32_t rb,
   return inc_n<L>(m, inc);
 }
 
+// (a2:a1:a0) += (b2:b1:b0)
+__device__ __forceinline__ void add3w(uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t b0,
+                                      uint32_t b1, uint32_t b2) {
+  asm("add.cc.u32 %0, %0, %3;\n\t"
+      "addc.cc.u32 %1, %1, %4;\n\t"
+      "addc.u32 %2, %2, %5;"
+      : "+r"(a0), "+r"(a1), "+r"(a2)
+      : "r"(b0), "r"(b1), "r"(b2));
+}
+
+// Independent accumulation chains per Comba column: the IMAD.WIDE of one
+// chain depends on the previous one through its 64-bit addend, so a single
+// chain per column serialises the whole product; NCH chains (merged at the
+// end of the column) give the scheduler NCH-way ILP at 3 adds per extra chain.
+template <int L>
+struct MulChains { static constexpr int n = L >= 32 ? 4 : (L >= 4 ? 2 : 1); };
+
 // --------------------------------------------------------------------------
 // t = RN_p(a * x).  a, x: L-limb mantissas (zero allowed: result zero).
 // Exponent of the result: ea + ex (top product bit set) or ea + ex - 1,
@@ -111,21 +128,32 @@ template <int L>
 __device__ __forceinline__ void mp_mul(const uint32_t (&a)[L], int32_t ea, uint32_t sa,
                                        const uint32_t (&x)[L], int32_t ex, uint32_t sx,
                                        MP<L>& t) {
+  constexpr int NCH = MulChains<L>::n;
   uint32_t c0 = 0u, c1 = 0u, c2 = 0u;
   uint32_t sticky = 0u, w = 0u;
   uint32_t P[L];
 #pragma unroll
   for (int k = 0; k < 2 * L - 1; ++k) {
+    const int ilo = k - (L - 1) > 0 ? k - (L - 1) : 0;
+    const int ihi = k < L - 1 ? k : L - 1;
+    const int nt = ihi - ilo + 1;                      // terms in column k
+    uint32_t A0[NCH], A1[NCH], A2[NCH];
+    A0[0] = c0; A1[0] = c1; A2[0] = c2;                // chain 0 carries the column-in
+#pragma unroll
+    for (int ch = 1; ch < NCH; ++ch) { A0[ch] = 0u; A1[ch] = 0u; A2[ch] = 0u; }
 #pragma unroll
     for (int i = 0; i < L; ++i) {
-      const int j = k - i;
-      if (j < 0 || j >= L) continue;
-      mac3(c0, c1, c2, a[i], x[j]);
+      if (i < ilo || i > ihi) continue;
+      const int ch = (i - ilo) % NCH;
+      mac3(A0[ch], A1[ch], A2[ch], a[i], x[k - i]);
     }
-    if (k < L - 1) sticky |= c0;           // columns 0..L-2: only "nonzero?" matters
-    else if (k == L - 1) w = c0;           // limb L-1: round bit(s) + sticky
-    else P[k - L] = c0;                    // limbs L..2L-2 of the product
-    c0 = c1; c1 = c2; c2 = 0u;
+#pragma unroll
+    for (int ch = 1; ch < NCH; ++ch)
+      if (ch < nt) add3w(A0[0], A1[0], A2[0], A0[ch], A1[ch], A2[ch]);
+    if (k < L - 1) sticky |= A0[0];        // columns 0..L-2: only "nonzero?" matters
+    else if (k == L - 1) w = A0[0];        // limb L-1: round bit(s) + sticky
+    else P[k - L] = A0[0];                 // limbs L..2L-2 of the product
+    c0 = A1[0]; c1 = A2[0]; c2 = 0u;
   }
   P[L - 1] = c0;                           // limb 2L-1
   // normalise: shift left by sh = 1 when the top product bit is clear

@@ -52,11 +52,14 @@ void parallel_for(int64_t n, F f) {
 }
 
 struct DevPart {
-  int64_t nrows = 0, nnz = 0, nslices = 0, nentries = 0, nlong = 0;
+  int64_t nrows = 0, nnz = 0, nslices = 0, nentries = 0, nwrow = 0;
   int32_t max_len = 0;
   int64_t* slice_ptr = nullptr;
   int32_t* slot_row = nullptr;
   int32_t* slot_len = nullptr;
+  int64_t* wrow_ptr = nullptr;
+  int32_t* wrow_row = nullptr;
+  int32_t* wrow_len = nullptr;
   int32_t* col = nullptr;
   int32_t* expw = nullptr;
   uint32_t* limbs = nullptr;
@@ -66,13 +69,16 @@ struct DevPart {
     PartView v;
     v.slice_ptr = slice_ptr; v.slot_row = slot_row; v.slot_len = slot_len;
     v.col = col; v.expw = expw; v.limbs = limbs;
-    v.nslices = nslices; v.nslots = nslices * 32; v.nlong = nlong;
+    v.nslices = nslices; v.nslots = nslices * 32;
+    v.nwrow = nwrow; v.wrow_ptr = wrow_ptr; v.wrow_row = wrow_row; v.wrow_len = wrow_len;
     return v;
   }
   void release() {
     cudaFree(slice_ptr); cudaFree(slot_row); cudaFree(slot_len);
+    cudaFree(wrow_ptr); cudaFree(wrow_row); cudaFree(wrow_len);
     cudaFree(col); cudaFree(expw); cudaFree(limbs);
     slice_ptr = nullptr; slot_row = nullptr; slot_len = nullptr;
+    wrow_ptr = nullptr; wrow_row = nullptr; wrow_len = nullptr;
     col = nullptr; expw = nullptr; limbs = nullptr;
   }
 };
@@ -121,16 +127,34 @@ int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32
   for (auto& c : cnt) { int64_t t = c; c = acc; acc += t; }
   std::vector<int32_t> order((size_t)nrows);
   for (int64_t r = 0; r < nrows; ++r) order[(size_t)cnt[(size_t)(maxlen - (lrp[r + 1] - lrp[r]))]++] = (int32_t)r;
-  const int64_t nslices = (nrows + 31) / 32;
+  // warp rows: the rows longer than the threshold (a prefix of `order`)
+  const int64_t T = long_row_threshold();
+  int64_t nw = 0;
+  while (nw < nrows && lrp[order[(size_t)nw] + 1] - lrp[order[(size_t)nw]] > T) ++nw;
+  P.nwrow = nw;
+  std::vector<int64_t> wptr((size_t)nw);
+  std::vector<int32_t> wrow((size_t)nw), wlen((size_t)nw);
+  int64_t ew = 0;
+  for (int64_t i = 0; i < nw; ++i) {
+    const int32_t r = order[(size_t)i];
+    wptr[(size_t)i] = ew;
+    wrow[(size_t)i] = r;
+    wlen[(size_t)i] = (int32_t)(lrp[r + 1] - lrp[r]);
+    ew += (wlen[(size_t)i] + 31) / 32 * 32;
+  }
+  // SELL slices of the remaining rows
+  const int64_t nshort = nrows - nw;
+  const int64_t nslices = (nshort + 31) / 32;
   P.nslices = nslices;
   std::vector<int64_t> sp((size_t)nslices + 1, 0);
   std::vector<int32_t> srow((size_t)nslices * 32, -1), slen((size_t)nslices * 32, 0);
+  sp[0] = ew;
   for (int64_t s = 0; s < nslices; ++s) {
     int64_t w = 0;
     for (int l = 0; l < 32; ++l) {
       int64_t slot = s * 32 + l;
-      if (slot < nrows) {
-        int32_t r = order[(size_t)slot];
+      if (slot < nshort) {
+        int32_t r = order[(size_t)(nw + slot)];
         srow[(size_t)slot] = r;
         slen[(size_t)slot] = (int32_t)(lrp[r + 1] - lrp[r]);
         w = std::max<int64_t>(w, slen[(size_t)slot]);
@@ -140,12 +164,6 @@ int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32
   }
   const int64_t nent = sp[(size_t)nslices];
   P.nentries = nent;
-  {
-    const int64_t T = long_row_threshold();
-    int64_t nl = 0;
-    while (nl < nslices && (sp[(size_t)nl + 1] - sp[(size_t)nl]) / 32 > T) ++nl;
-    P.nlong = nl;
-  }
   const int CW = L < 4 ? L : 4, NC = L / CW;
   // --- a1: repack (host), zero-filled padding
   std::vector<int32_t> hcol, hexp;
@@ -157,6 +175,25 @@ int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32
   } catch (const std::bad_alloc&) {
     return MPSP_E_NOMEM;
   }
+  // entry E <- local entry e: column, packed exponent word, chunk-major limbs
+  auto put = [&](int64_t E, int64_t e) {
+    const int64_t k = srck ? srck[e] : k0 + e;    // source entry
+    const int64_t g = E / 32;
+    const int l = (int)(E % 32);
+    hcol[(size_t)E] = lcol[e];
+    const uint32_t* src = limbs + (size_t)k * L;
+    const bool nz = src[L - 1] != 0u;
+    hexp[(size_t)E] = nz ? (int32_t)(((uint32_t)signs[k] << 31) | ((uint32_t)exps[k] & 0x7fffffffu)) : 0;
+    for (int c = 0; c < NC; ++c)
+      for (int w = 0; w < CW; ++w)
+        hl[(size_t)(((g * NC + c) * 32 + l) * CW + w)] = nz ? src[c * CW + w] : 0u;
+  };
+  parallel_for(nw, [&](int64_t i0, int64_t i1) {
+    for (int64_t i = i0; i < i1; ++i) {
+      const int32_t r = wrow[(size_t)i];
+      for (int64_t j = 0; j < wlen[(size_t)i]; ++j) put(wptr[(size_t)i] + j, lrp[r] + j);
+    }
+  });
   parallel_for(nslices, [&](int64_t s0, int64_t s1) {
     for (int64_t s = s0; s < s1; ++s) {
       for (int l = 0; l < 32; ++l) {
@@ -164,19 +201,7 @@ int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32
         const int32_t r = srow[(size_t)slot];
         if (r < 0) continue;
         const int64_t len = slen[(size_t)slot];
-        for (int64_t j = 0; j < len; ++j) {
-          const int64_t e = lrp[r] + j;                 // local entry
-          const int64_t k = srck ? srck[e] : k0 + e;    // source entry
-          const int64_t g = sp[(size_t)s] / 32 + j;
-          const int64_t E = g * 32 + l;
-          hcol[(size_t)E] = lcol[e];
-          const uint32_t* src = limbs + (size_t)k * L;
-          bool nz = src[L - 1] != 0u;
-          hexp[(size_t)E] = nz ? (int32_t)(((uint32_t)signs[k] << 31) | ((uint32_t)exps[k] & 0x7fffffffu)) : 0;
-          for (int c = 0; c < NC; ++c)
-            for (int w = 0; w < CW; ++w)
-              hl[(size_t)(((g * NC + c) * 32 + l) * CW + w)] = nz ? src[c * CW + w] : 0u;
-        }
+        for (int64_t j = 0; j < len; ++j) put((sp[(size_t)s] / 32 + j) * 32 + l, lrp[r] + j);
       }
     }
   });
@@ -196,6 +221,9 @@ int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32
   if ((rc = up((void**)&P.slice_ptr, sp.data(), sp.size() * 8)) ||
       (rc = up((void**)&P.slot_row, srow.data(), srow.size() * 4)) ||
       (rc = up((void**)&P.slot_len, slen.data(), slen.size() * 4)) ||
+      (rc = up((void**)&P.wrow_ptr, wptr.data(), wptr.size() * 8)) ||
+      (rc = up((void**)&P.wrow_row, wrow.data(), wrow.size() * 4)) ||
+      (rc = up((void**)&P.wrow_len, wlen.data(), wlen.size() * 4)) ||
       (rc = up((void**)&P.col, hcol.data(), hcol.size() * 4)) ||
       (rc = up((void**)&P.expw, hexp.data(), hexp.size() * 4)) ||
       (rc = up((void**)&P.limbs, hl.data(), hl.size() * 4)))
@@ -280,7 +308,7 @@ int do_spmv(const mpsp_csr* A, bool transpose, const uint32_t* xl, const int32_t
   XView xv{xl, xe, xs};
   YView yv{yl, ye, ys};
   const PartView pv = P.view();
-  const bool has_long = pv.nlong > 0, has_short = pv.nslots > pv.nlong * 32;
+  const bool has_long = pv.nwrow > 0, has_short = pv.nslots > 0;
   if (has_long && has_short && A->aux) {
     // long rows on the aux stream (started first: they are the critical
     // path), short rows on the caller's stream, joined back on the caller's
@@ -412,7 +440,7 @@ int mpsp_csr_create(mpsp_csr** out, int p_bits, int64_t n, const int64_t* rowptr
       rc = MPSP_E_NOMEM;
     }
   }
-  if (rc == MPSP_OK && (H->A.nlong > 0 || H->T.nlong > 0)) {
+  if (rc == MPSP_OK && (H->A.nwrow > 0 || H->T.nwrow > 0)) {
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
     if ((ce = cudaStreamCreateWithPriority(&H->aux, cudaStreamNonBlocking, prio_hi)) != cudaSuccess ||

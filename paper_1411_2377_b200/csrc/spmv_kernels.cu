@@ -24,7 +24,7 @@ void launch_counter_add(int64_t k) { g_launches.fetch_add(k); }
 
 template <int L, int MINB>
 __global__ void __launch_bounds__(128, MINB) spmv_sell(PartView P, XView x, YView y) {
-  const int64_t slot = P.nlong * 32 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (slot >= P.nslots) return;
   const int row = P.slot_row[slot];
   if (row < 0) return;
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(128, MINB) spmv_sell(PartView P, XView x, YVie
 
 template <int L>
 static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStream_t st) {
-  const int64_t nshort = P.nslots - P.nlong * 32;
+  const int64_t nshort = P.nslots;
   if (nshort <= 0) return 0;
   const int threads = 128;
   const int64_t blocks = (nshort + threads - 1) / threads;

@@ -1,0 +1,298 @@
+// spmv_wrow.cu - one warp per long row: products in parallel across the
+// lanes, and the ordered rounded add chain evaluated 32 steps at a time by an
+// EXACT speculative block sum (hard part 2: the chain
+// s = RN(s + t_k) of a 5000-long C4 row is a serial critical path).
+//
+// Why a block of steps can be summed in parallel.  Let s have exponent E, so
+// s = S*u with u = 2^(E-p) and S an integer in [2^(p-1), 2^p).  If the exact
+// value V = s + t_k lies in the same binade and its rounding stays below 2^E,
+// RN_p(s + t_k) = (S + RN_int(t_k/u)) * u: the rounding grid is u, and s is on
+// it.  So while the partial sums stay in one binade, the chain is the integer
+// sum  S_k = S_{k-1} + Q_k  with Q_k = +-RN_int(|t_k|/u)  - associative, i.e.
+// computable in any order.  RN_int's only dependence on the running sum is the
+// tie case (|t_k|/u = m + 1/2 exactly: round to the EVEN S_k), which needs the
+// parity of S_{k-1}; parities are prefix XORs of the Q_k's low bits and a tie
+// resets the parity to 0, so every lane gets its own in O(1) from two ballots.
+//
+// Per block of 32 entries (one per lane): each lane forms t_k = RN(a_k x_col)
+// (Comba, IMAD.WIDE), aligns it to the grid u, and rounds it (Q_k).  A warp
+// scan of 64-bit high parts h_k = floor(Q_k/H) gives conservative bounds on
+// every partial sum; if all are provably inside [2^(p-1), 2^p - 1] the block
+// commits: each lane adds Q_k to its private (L+2)-limb partial sum R_lane
+// (S = sum over lanes of R, exact mod 2^(32(L+2)), reduced only when needed).
+// Otherwise, at the first failing step f, the steps before f commit, S is
+// reduced exactly (warp butterfly), step f is done by the general adder
+// mp_add (all lanes redundantly), and the block resumes at f+1 with the new
+// binade.  Nothing is approximated: the bounds only decide fast vs exact.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+
+#include "kernel_common.cuh"
+
+namespace mpsp {
+
+// Read at every mpsp_csr_create: rows longer than this go to spmv_wrow
+// (tests lower it to route rows of any length through this kernel).
+int long_row_threshold() {
+  const char* v = std::getenv("MPSP_LONG_T");
+  return v ? std::atoi(v) : 32;
+}
+
+// High-part scale H: S/H in [2^(HB-1), 2^HB).  HB = 56 keeps a 32-lane scan
+// of |h| <= 2^55 far from int64 overflow.
+constexpr int HB = 56;
+
+template <int L>
+__device__ __forceinline__ int64_t hi_of_mant(const uint32_t (&m)[L]) {
+  if constexpr (L == 1) {
+    return (int64_t)m[0] << (HB - 32);
+  } else {
+    return (int64_t)((((uint64_t)m[L - 1] << 32) | m[L - 2]) >> (64 - HB));
+  }
+}
+
+// floor(Q / H) for an (L+2)-limb two's complement Q with |Q| <= 2^(p-1) + 1
+template <int L>
+__device__ __forceinline__ int64_t hi_of_q(const uint32_t (&Q)[L + 2]) {
+  if constexpr (L == 1) {
+    const int64_t v = (int64_t)(((uint64_t)Q[1] << 32) | Q[0]);
+    return v * ((int64_t)1 << (HB - 32));
+  } else {
+    const uint32_t lo = __funnelshift_r(Q[L - 2], Q[L - 1], 64 - HB);
+    const uint32_t hi = __funnelshift_r(Q[L - 1], Q[L], 64 - HB);
+    return (int64_t)(((uint64_t)hi << 32) | lo);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void warp_sum_limbs(uint32_t (&S)[N]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uint32_t T[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) T[i] = __shfl_xor_sync(0xffffffffu, S[i], o);
+    add_n<N>(S, S, T);
+  }
+}
+
+template <int L>
+struct WPrefetch { static constexpr bool on = (L <= 16); };
+
+template <int L>
+struct WEntry {
+  uint32_t a[L], x[L];
+  int32_t w, ex;
+  uint32_t sx;
+  bool valid;
+};
+
+template <int L>
+__device__ __forceinline__ void wload(const PartView& P, const XView& x, int64_t e0, int jb,
+                                      int len, int lane, WEntry<L>& E) {
+  const int j = jb + lane;
+  E.valid = j < len;
+  if (!E.valid) {
+#pragma unroll
+    for (int i = 0; i < L; ++i) { E.a[i] = 0u; E.x[i] = 0u; }
+    E.w = 0; E.ex = 0; E.sx = 0u;
+    return;
+  }
+  const int64_t e = e0 + j;
+  const int col = __ldg(P.col + e);
+  E.w = __ldg(P.expw + e);
+  load_a<L>(P.limbs, e >> 5, lane, E.a);
+  load_x<L>(x.limbs, col, E.x);
+  E.ex = __ldg(x.exps + col);
+  E.sx = __ldg(x.signs + col);
+}
+
+template <int L>
+__global__ void __launch_bounds__(128) spmv_wrow(PartView P, XView x, YView y) {
+  constexpr int N = L + 2;
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int64_t LO = (int64_t)1 << (HB - 1), HI = (int64_t)1 << HB;
+  constexpr int64_t M1 = (L == 1) ? ((int64_t)1 << (HB - 32)) : 1;   // one grid unit u, in H
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= P.nwrow) return;
+  const int64_t e0 = P.wrow_ptr[w];
+  const int len = P.wrow_len[w];
+  const int row = P.wrow_row[w];
+  const unsigned below = (1u << lane) - 1u;
+
+  uint32_t R[N];                      // this lane's share of S (two's complement)
+#pragma unroll
+  for (int i = 0; i < N; ++i) R[i] = 0u;
+  bool szero = true;                  // accumulator is exactly zero (warp-uniform)
+  int32_t E = 0;                      // accumulator exponent (warp-uniform)
+  uint32_t sg = 0u;                   // accumulator sign
+  int64_t Shi = 0, err = 0;           // S/H in [Shi, Shi + err)
+  uint32_t par = 0u;                  // parity of S
+
+  WEntry<L> nxt;
+  if (WPrefetch<L>::on) wload<L>(P, x, e0, 0, len, lane, nxt);
+  for (int jb = 0; jb < len; jb += 32) {
+    MP<L> t;
+    {
+      WEntry<L> cur;
+      if constexpr (WPrefetch<L>::on) {
+        cur = nxt;
+        if (jb + 32 < len) wload<L>(P, x, e0, jb + 32, len, lane, nxt);
+      } else {
+        wload<L>(P, x, e0, jb, len, lane, cur);
+      }
+      const int32_t ea = (int32_t)((uint32_t)cur.w << 1) >> 1;
+      mp_mul<L>(cur.a, ea, (uint32_t)cur.w >> 31, cur.x, cur.ex, cur.sx, t);
+    }
+    const bool tz = t.is_zero();       // padding lanes have zero limbs
+    int start = 0;
+    while (start < 32) {
+      if (szero) {
+        // s = +0: the first nonzero product is absorbed exactly
+        const unsigned nzm = __ballot_sync(FULL, !tz && lane >= start);
+        if (nzm == 0u) break;
+        const int f = __ffs(nzm) - 1;
+        uint32_t m[L];
+#pragma unroll
+        for (int i = 0; i < L; ++i) m[i] = __shfl_sync(FULL, t.m[i], f);
+        E = __shfl_sync(FULL, t.e, f);
+        sg = __shfl_sync(FULL, t.s, f);
+#pragma unroll
+        for (int i = 0; i < N; ++i) R[i] = (lane == 0 && i < L) ? m[i] : 0u;
+        Shi = hi_of_mant<L>(m);
+        err = 1;
+        par = m[0] & 1u;
+        szero = false;
+        start = f + 1;
+        continue;
+      }
+      const bool act = (lane >= start) && !tz;
+      const int64_t d64 = (int64_t)E - (int64_t)t.e;
+      const bool badd = act && d64 < 1;              // |t| >= 2^(E-1): leaves the binade
+      const bool use = act && !badd;
+      const uint32_t dd = use ? (uint32_t)min(d64, (int64_t)(32 * L + 32)) : 0u;
+      // Y = |t| / u  as integer limbs Y[1..L] and guard limb Y[0]
+      uint32_t Y[L + 1];
+      Y[0] = 0u;
+#pragma unroll
+      for (int i = 0; i < L; ++i) Y[i + 1] = t.m[i];
+      uint32_t stk = 0u;
+      shr_bits_sticky<L + 1>(Y, dd, stk);
+      const uint32_t rb = Y[0] >> 31;
+      const bool sticky = (stk | (Y[0] << 1)) != 0u;
+      const bool tie = use && rb && !sticky;
+      uint32_t inc = (rb && sticky) ? 1u : 0u;
+      const uint32_t lsbY = Y[1] & 1u;
+      const unsigned actM = __ballot_sync(FULL, act);
+      const unsigned tieM = __ballot_sync(FULL, tie);
+      const unsigned bM = __ballot_sync(FULL, use && !tie && ((lsbY ^ inc) & 1u));
+      if (tie) {
+        // parity of S_{k-1}: reset to 0 by the last tie before k, then the
+        // XOR of the non-tie Q_j low bits since
+        const unsigned tb = tieM & below;
+        const int lt = tb ? 31 - __clz(tb) : -1;
+        const unsigned seg = below & (lt >= 0 ? ~((2u << lt) - 1u) : FULL);
+        const uint32_t pS = ((lt >= 0 ? 0u : par) ^ (uint32_t)__popc(bM & seg)) & 1u;
+        inc = pS ^ lsbY;                              // make S_k even
+      }
+      // Q = +-(Y + inc) in N-limb two's complement
+      uint32_t Q[N];
+#pragma unroll
+      for (int i = 0; i < L; ++i) Q[i] = use ? Y[i + 1] : 0u;
+      Q[L] = 0u;
+      Q[L + 1] = 0u;
+      inc_n<N>(Q, use ? inc : 0u);
+      const uint32_t neg = (use && t.s != sg) ? 1u : 0u;
+      const uint32_t nm = 0u - neg;
+#pragma unroll
+      for (int i = 0; i < N; ++i) Q[i] ^= nm;
+      inc_n<N>(Q, neg);
+      const int64_t h = hi_of_q<L>(Q);
+      int64_t Pi = h;                                 // inclusive scan of h
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t v = __shfl_up_sync(FULL, Pi, o);
+        if (lane >= o) Pi += v;
+      }
+      const int64_t LB = Shi + (Pi - h);              // S_{k-1}/H >= LB
+      const int64_t ek = err + __popc(actM & below);  // S_{k-1}/H < LB + ek
+      const bool ok = !act || (!badd && LB + h - M1 >= LO && LB + ek + h + 1 <= HI);
+      const unsigned failM = __ballot_sync(FULL, !ok);
+      if (failM == 0u) {
+        add_n<N>(R, R, Q);
+        Shi += __shfl_sync(FULL, Pi, 31);
+        err += __popc(actM);
+        const int lt = tieM ? 31 - __clz(tieM) : -1;
+        const unsigned seg = lt >= 0 ? ~((2u << lt) - 1u) : FULL;
+        par = ((lt >= 0 ? 0u : par) ^ (uint32_t)__popc(bM & seg)) & 1u;
+        break;
+      }
+      // ---- exact path at the first failing step f
+      const int f = __ffs(failM) - 1;
+      if (lane < f) add_n<N>(R, R, Q);               // steps before f are valid
+      uint32_t S[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) S[i] = R[i];
+      warp_sum_limbs<N>(S);
+      MP<L> s, tf;
+#pragma unroll
+      for (int i = 0; i < L; ++i) {
+        s.m[i] = S[i];
+        tf.m[i] = __shfl_sync(FULL, t.m[i], f);
+      }
+      s.e = E;
+      s.s = sg;
+      tf.e = __shfl_sync(FULL, t.e, f);
+      tf.s = __shfl_sync(FULL, t.s, f);
+      mp_add<L>(s, tf);
+      szero = s.is_zero();
+#pragma unroll
+      for (int i = 0; i < N; ++i) R[i] = (lane == 0 && i < L) ? s.m[i] : 0u;
+      E = s.e;
+      sg = s.s;
+      Shi = szero ? 0 : hi_of_mant<L>(s.m);
+      err = 1;
+      par = s.m[0] & 1u;
+      start = f + 1;
+    }
+  }
+  MP<L> s;
+  {
+    uint32_t S[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) S[i] = R[i];
+    warp_sum_limbs<N>(S);
+#pragma unroll
+    for (int i = 0; i < L; ++i) s.m[i] = szero ? 0u : S[i];
+  }
+  s.e = E;
+  s.s = sg;
+  if (lane == 0 && row >= 0) store_y<L>(y, row, s);
+}
+
+template <int L>
+static int launch_wrow_L(const PartView& P, const XView& x, const YView& y, cudaStream_t st) {
+  if (P.nwrow <= 0) return 0;
+  const int threads = 128;
+  const int64_t blocks = (P.nwrow * 32 + threads - 1) / threads;
+  spmv_wrow<L><<<(unsigned)blocks, threads, 0, st>>>(P, x, y);
+  launch_counter_add(1);
+  return (int)cudaGetLastError();
+}
+
+int launch_spmv_long(int L, const PartView& P, const XView& x, const YView& y, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (L) {
+    case 1: return launch_wrow_L<1>(P, x, y, st);
+    case 2: return launch_wrow_L<2>(P, x, y, st);
+    case 4: return launch_wrow_L<4>(P, x, y, st);
+    case 8: return launch_wrow_L<8>(P, x, y, st);
+    case 16: return launch_wrow_L<16>(P, x, y, st);
+    case 32: return launch_wrow_L<32>(P, x, y, st);
+    default: return (int)cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace mpsp
