@@ -35,15 +35,18 @@ def _deps_mtime() -> float:
     return max(m, os.path.getmtime(__file__))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _deps_mtime():
-        return LIB
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), name: str = "libmpsp.so") -> str:
+    """Compile the library; `defines`/`name` build a tuning variant beside it."""
+    lib = os.path.join(PKG, name)
+    if not force and os.path.exists(lib) and os.path.getmtime(lib) >= _deps_mtime():
+        return lib
+    bdir = BUILD if name == "libmpsp.so" else os.path.join(BUILD, name)
+    os.makedirs(bdir, exist_ok=True)
     nv = nvcc()
 
     def compile_one(src):
-        obj = os.path.join(BUILD, src + ".o")
-        cmd = [nv, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(bdir, src + ".o")
+        cmd = [nv, *ARCH, *FLAGS, *defines, "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -55,14 +58,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [nv, *ARCH, "-shared", "--cudart", "shared", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a for a in sys.argv[1:] if a.startswith("-D")]
+    names = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--name=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs,
+                name=names[0] if names else "libmpsp.so"))

@@ -8,7 +8,8 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libmpsp.so")
+# MPSP_LIB selects an in-tree tuning variant (tools/variants.sh); default libmpsp.so
+LIB_PATH = os.path.join(_PKG, os.environ.get("MPSP_LIB", "libmpsp.so"))
 
 MPSP_OK = 0
 MPSP_WITH_TRANSPOSE = 0x1

@@ -116,8 +116,12 @@ __device__ __forceinline__ void add3w(uint32_t& a0, uint32_t& a1, uint32_t& a2, 
 // chain depends on the previous one through its 64-bit addend, so a single
 // chain per column serialises the whole product; NCH chains (merged at the
 // end of the column) give the scheduler NCH-way ILP at 3 adds per extra chain.
+// (measured on B200: 2 chains best at L = 16, 32; 1 at L <= 8)
+#ifndef MPSP_NCH
+#define MPSP_NCH 2
+#endif
 template <int L>
-struct MulChains { static constexpr int n = L >= 32 ? 4 : (L >= 4 ? 2 : 1); };
+struct MulChains { static constexpr int n = L >= 16 ? MPSP_NCH : 1; };
 
 // --------------------------------------------------------------------------
 // t = RN_p(a * x).  a, x: L-limb mantissas (zero allowed: result zero).
@@ -125,9 +129,9 @@ struct MulChains { static constexpr int n = L >= 32 ? 4 : (L >= 4 ? 2 : 1); };
 // +1 if rounding carried out.
 // --------------------------------------------------------------------------
 template <int L>
-__device__ __forceinline__ void mp_mul(const uint32_t (&a)[L], int32_t ea, uint32_t sa,
-                                       const uint32_t (&x)[L], int32_t ex, uint32_t sx,
-                                       MP<L>& t) {
+__device__ __forceinline__ void mp_mul_full(const uint32_t (&a)[L], int32_t ea, uint32_t sa,
+                                            const uint32_t (&x)[L], int32_t ex, uint32_t sx,
+                                            MP<L>& t) {
   constexpr int NCH = MulChains<L>::n;
   uint32_t c0 = 0u, c1 = 0u, c2 = 0u;
   uint32_t sticky = 0u, w = 0u;
@@ -168,6 +172,111 @@ __device__ __forceinline__ void mp_mul(const uint32_t (&a)[L], int32_t ea, uint3
   if (cy) t.m[L - 1] = 0x80000000u;
   t.e = ea + ex - (int32_t)sh + (int32_t)cy;
   t.s = sa ^ sx;
+}
+
+// Columns [K0, 2L-2] of the Comba product from a zero carry-in: T[m - K0] =
+// limb m of  sum_{i+j >= K0} a_i x_j 2^(32(i+j))  for m in [K0, 2L-1].
+template <int L, int K0>
+__device__ __forceinline__ void comba_upper(const uint32_t (&a)[L], const uint32_t (&x)[L],
+                                            uint32_t (&T)[2 * L - K0]) {
+  constexpr int NCH = MulChains<L>::n;
+  uint32_t c0 = 0u, c1 = 0u, c2 = 0u;
+#pragma unroll
+  for (int k = K0; k < 2 * L - 1; ++k) {
+    const int ilo = k - (L - 1) > 0 ? k - (L - 1) : 0;
+    const int ihi = k < L - 1 ? k : L - 1;
+    const int nt = ihi - ilo + 1;
+    uint32_t A0[NCH], A1[NCH], A2[NCH];
+    A0[0] = c0; A1[0] = c1; A2[0] = c2;
+#pragma unroll
+    for (int ch = 1; ch < NCH; ++ch) { A0[ch] = 0u; A1[ch] = 0u; A2[ch] = 0u; }
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      if (i < ilo || i > ihi) continue;
+      const int ch = (i - ilo) % NCH;
+      mac3(A0[ch], A1[ch], A2[ch], a[i], x[k - i]);
+    }
+#pragma unroll
+    for (int ch = 1; ch < NCH; ++ch)
+      if (ch < nt) add3w(A0[0], A1[0], A2[0], A0[ch], A1[ch], A2[ch]);
+    T[k - K0] = A0[0];
+    c0 = A1[0]; c1 = A2[0]; c2 = 0u;
+  }
+  T[2 * L - 1 - K0] = c0;
+}
+
+// Columns [0, K0) of the Comba product: returns the OR of limbs 0..K0-1
+// (sticky) and the carry (c0, c1, c2) into column K0.
+template <int L, int K0>
+__device__ __forceinline__ uint32_t comba_lower(const uint32_t (&a)[L], const uint32_t (&x)[L],
+                                                uint32_t& c0, uint32_t& c1, uint32_t& c2) {
+  uint32_t sticky = 0u;
+  c0 = 0u; c1 = 0u; c2 = 0u;
+#pragma unroll
+  for (int k = 0; k < K0; ++k) {
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      if (i > k || k - i >= L) continue;
+      mac3(c0, c1, c2, a[i], x[k - i]);
+    }
+    sticky |= c0;
+    c0 = c1; c1 = c2; c2 = 0u;
+  }
+  return sticky;
+}
+
+// --------------------------------------------------------------------------
+// t = RN_p(a * x) by a SHORT product with an exactness certificate (DESIGN.md
+// "Product").  Only columns k >= K0 = L-3 are formed first (T); the omitted
+// part N = sum_{i+j<K0} a_i x_j 2^(32(i+j)) satisfies 0 <= N < 2^B,
+// B = 32(L-2)+5 (K0 < 32 terms per column, each < 2^64).  Let W be the bits
+// of T in [B, round bit).  If W is neither all zeros nor all ones, adding N
+// cannot carry past W, so every bit from the round bit up - hence the
+// normalisation, the kept limbs and the round bit - is the exact product's,
+// and the sticky is 1 (W or W+1 is nonzero).  Otherwise (probability ~2^-56
+// on random mantissas; common only for structured inputs) the lower columns
+// are formed too and their carry added in: the exact product.
+// Executed limb-MACs on the fast path: L^2 - (L-3)(L-2)/2 (L=32: 618 of 1024).
+// --------------------------------------------------------------------------
+template <int L>
+__device__ __forceinline__ void mp_mul(const uint32_t (&a)[L], int32_t ea, uint32_t sa,
+                                       const uint32_t (&x)[L], int32_t ex, uint32_t sx,
+                                       MP<L>& t) {
+  if constexpr (L < 4) {
+    mp_mul_full<L>(a, ea, sa, x, ex, sx, t);
+  } else {
+    constexpr int K0 = L - 3;
+    uint32_t T[L + 3];                               // limbs L-3 .. 2L-1
+    comba_upper<L, K0>(a, x, T);
+    uint32_t sh = (~T[L + 2]) >> 31;                 // top product bit clear -> 1
+    const uint32_t wmask = (1u << (31u - sh)) - 1u;  // T[2] bits below the round bit
+    const uint32_t w1 = T[1] >> 5, w2 = T[2] & wmask;
+    const bool amb = ((w1 | w2) == 0u) || (w1 == 0x07FFFFFFu && w2 == wmask);
+    const bool zero = (a[L - 1] == 0u) || (x[L - 1] == 0u);
+    uint32_t stk = 1u;
+    if (amb && !zero) {                              // rare: complete the product
+      uint32_t c0, c1, c2;
+      const uint32_t slo = comba_lower<L, K0>(a, x, c0, c1, c2);
+      uint32_t C[L + 3];
+      C[0] = c0; C[1] = c1; C[2] = c2;
+#pragma unroll
+      for (int i = 3; i < L + 3; ++i) C[i] = 0u;
+      add_n<L + 3>(T, T, C);
+      sh = (~T[L + 2]) >> 31;
+      stk = slo | T[0] | T[1] | ((T[2] << sh) << 1);
+    }
+#pragma unroll
+    for (int i = L - 1; i >= 0; --i) t.m[i] = __funnelshift_l(T[i + 2], T[i + 3], sh);
+    const uint32_t rb = (T[2] << sh) >> 31;
+    const uint32_t cy = rne_increment<L>(t.m, rb, stk);
+    if (cy) t.m[L - 1] = 0x80000000u;
+    t.e = ea + ex - (int32_t)sh + (int32_t)cy;
+    t.s = sa ^ sx;
+    if (zero) {
+#pragma unroll
+      for (int i = 0; i < L; ++i) t.m[i] = 0u;
+    }
+  }
 }
 
 // --------------------------------------------------------------------------
