@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--op", default="ax", choices=["ax", "atx"])
     ap.add_argument("--impl", default="mpsp", choices=["mpsp", "reference"])
+    ap.add_argument("--exchange", default="window", choices=["window", "allgather"],
+                    help="x exchange for N > 1 (dist.py)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
@@ -191,7 +193,7 @@ def main():
     __graft_entry__.build()
     import gen
     from paper_1411_2377_b200 import CSR, MPVec, launch_count, imad_bench
-    from paper_1411_2377_b200.dist import block_range, allgather_x
+    from paper_1411_2377_b200.dist import block_range, allgather_x, needed_window, WindowExchange
 
     t0 = time.perf_counter()
     d = gen.make(args.config, seed=args.seed)
@@ -208,6 +210,13 @@ def main():
     x_full_host = (d["x_limbs"], d["x_exps"], d["x_signs"])
     x_local = MPVec.from_host(d["x_limbs"][rb:re], d["x_exps"][rb:re], d["x_signs"][rb:re], device=dev)
     x_full = MPVec.from_host(*x_full_host, device=dev) if world == 1 else None
+    X = None
+    if world > 1 and args.exchange == "window":
+        win = needed_window(d["rowptr"], d["colidx"], rb, re, transpose=(args.op == "atx"))
+        X = WindowExchange(n, L, win, device=dev)
+        v = X.local_view()                 # x_local lives in the exchange buffer
+        v.limbs.copy_(x_local.limbs); v.exps.copy_(x_local.exps); v.signs.copy_(x_local.signs)
+        x_local = v
     y = MPVec.empty(re - rb, L, device=dev)
     f = A.spmv if args.op == "ax" else A.spmv_t
     stream = torch.cuda.current_stream(dev)
@@ -218,7 +227,12 @@ def main():
     flush_buf = torch.empty(int(2 * L2_BYTES), dtype=torch.uint8, device=dev) if flush else None
 
     def step():
-        xf = x_full if world == 1 else allgather_x(x_local, n)
+        if world == 1:
+            xf = x_full
+        elif X is not None:
+            xf = X.exchange(x_local)
+        else:
+            xf = allgather_x(x_local, n)
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
@@ -343,7 +357,9 @@ def main():
         "data": "synthetic",
         "config": {"workload": f"{args.config} {args.op}", "n": n, "nnz": nnz_all, "p": p,
                    "max_row": d["meta"]["max_row"], "seed": args.seed,
-                   "parallelism": f"row-block x{world}" + (" + NCCL all-gather of x" if world > 1 else ""),
+                   "parallelism": f"row-block x{world}" + (
+                       "" if world == 1 else (" + NCCL all-gather of x" if X is None else
+                                              " + NCCL P2P needed-window exchange of x")),
                    "l2": "flushed between steps (2x L2 memset outside step events)" if flush
                    else "inputs larger than L2"},
         "limb_macs_per_s": macs_full / (ms_per_step * 1e-3),

@@ -41,9 +41,10 @@ __global__ void __launch_bounds__(128, MINB) spmv_sell(PartView P, XView x, YVie
   uint32_t s0 = 0, s1 = 0;
   const int32_t* colp = P.col + g0 * 32 + l;
   const int32_t* expp = P.expw + g0 * 32 + l;
-  auto fetch = [&](int j, uint32_t (&a)[L], uint32_t (&xv)[L], int32_t& w, int32_t& ex,
-                   uint32_t& sx) {
-    const int col = __ldg(colp + 32 * j);
+  // The x gather of entry j depends on col[j]: columns are loaded one entry
+  // earlier than the rest of the entry, so the gather never waits on them.
+  auto fetch = [&](int j, int col, uint32_t (&a)[L], uint32_t (&xv)[L], int32_t& w,
+                   int32_t& ex, uint32_t& sx) {
     w = __ldg(expp + 32 * j);
     load_a<L>(P.limbs, g0 + j, l, a);
     load_x<L>(x.limbs, col, xv);
@@ -57,12 +58,24 @@ __global__ void __launch_bounds__(128, MINB) spmv_sell(PartView P, XView x, YVie
     mp_mul<L>(a, ea, (uint32_t)w >> 31, xv, ex, sx, t);
     mp_add<L>(s, t);
   };
-  if (len > 0) fetch(0, a0, x0, w0, e0, s0);
+  int cnext = 0;                          // column of the next entry to fetch
+  if (len > 0) {
+    fetch(0, __ldg(colp), a0, x0, w0, e0, s0);
+    if (len > 1) cnext = __ldg(colp + 32);
+  }
   for (int j = 0; j < len; j += 2) {
-    if (j + 1 < len) fetch(j + 1, a1, x1, w1, e1, s1);
+    if (j + 1 < len) {
+      const int c = cnext;
+      if (j + 2 < len) cnext = __ldg(colp + 32 * (j + 2));
+      fetch(j + 1, c, a1, x1, w1, e1, s1);
+    }
     step(a0, x0, w0, e0, s0);
     if (j + 1 >= len) break;
-    if (j + 2 < len) fetch(j + 2, a0, x0, w0, e0, s0);
+    if (j + 2 < len) {
+      const int c = cnext;
+      if (j + 3 < len) cnext = __ldg(colp + 32 * (j + 3));
+      fetch(j + 2, c, a0, x0, w0, e0, s0);
+    }
     step(a1, x1, w1, e1, s1);
   }
   store_y<L>(y, row, s);

@@ -37,7 +37,7 @@ namespace mpsp {
 // (tests lower it to route rows of any length through this kernel).
 int long_row_threshold() {
   const char* v = std::getenv("MPSP_LONG_T");
-  return v ? std::atoi(v) : 32;
+  return v ? std::atoi(v) : 128;
 }
 
 // High-part scale H: S/H in [2^(HB-1), 2^HB).  HB = 56 keeps a 32-lane scan
@@ -88,9 +88,11 @@ struct WEntry {
   bool valid;
 };
 
+// Entry jb + lane of the row; its column `col` was loaded one block earlier
+// (the x gather never waits on the column load).
 template <int L>
 __device__ __forceinline__ void wload(const PartView& P, const XView& x, int64_t e0, int jb,
-                                      int len, int lane, WEntry<L>& E) {
+                                      int len, int lane, int col, WEntry<L>& E) {
   const int j = jb + lane;
   E.valid = j < len;
   if (!E.valid) {
@@ -100,12 +102,15 @@ __device__ __forceinline__ void wload(const PartView& P, const XView& x, int64_t
     return;
   }
   const int64_t e = e0 + j;
-  const int col = __ldg(P.col + e);
   E.w = __ldg(P.expw + e);
   load_a<L>(P.limbs, e >> 5, lane, E.a);
   load_x<L>(x.limbs, col, E.x);
   E.ex = __ldg(x.exps + col);
   E.sx = __ldg(x.signs + col);
+}
+
+__device__ __forceinline__ int wcol(const PartView& P, int64_t e0, int jb, int len, int lane) {
+  return (jb + lane < len) ? __ldg(P.col + e0 + jb + lane) : 0;
 }
 
 template <int L>
@@ -132,16 +137,26 @@ __global__ void __launch_bounds__(128) spmv_wrow(PartView P, XView x, YView y) {
   uint32_t par = 0u;                  // parity of S
 
   WEntry<L> nxt;
-  if (WPrefetch<L>::on) wload<L>(P, x, e0, 0, len, lane, nxt);
+  int cnext = 0;                      // columns of the block after the prefetched one
+  if (WPrefetch<L>::on) {
+    wload<L>(P, x, e0, 0, len, lane, wcol(P, e0, 0, len, lane), nxt);
+    cnext = wcol(P, e0, 32, len, lane);
+  } else {
+    cnext = wcol(P, e0, 0, len, lane);
+  }
   for (int jb = 0; jb < len; jb += 32) {
     MP<L> t;
     {
       WEntry<L> cur;
       if constexpr (WPrefetch<L>::on) {
         cur = nxt;
-        if (jb + 32 < len) wload<L>(P, x, e0, jb + 32, len, lane, nxt);
+        if (jb + 32 < len) {
+          wload<L>(P, x, e0, jb + 32, len, lane, cnext, nxt);
+          cnext = wcol(P, e0, jb + 64, len, lane);
+        }
       } else {
-        wload<L>(P, x, e0, jb, len, lane, cur);
+        wload<L>(P, x, e0, jb, len, lane, cnext, cur);
+        cnext = wcol(P, e0, jb + 32, len, lane);
       }
       const int32_t ea = (int32_t)((uint32_t)cur.w << 1) >> 1;
       mp_mul<L>(cur.a, ea, (uint32_t)cur.w >> 31, cur.x, cur.ex, cur.sx, t);
@@ -197,18 +212,16 @@ __global__ void __launch_bounds__(128) spmv_wrow(PartView P, XView x, YView y) {
         const uint32_t pS = ((lt >= 0 ? 0u : par) ^ (uint32_t)__popc(bM & seg)) & 1u;
         inc = pS ^ lsbY;                              // make S_k even
       }
-      // Q = +-(Y + inc) in N-limb two's complement
-      uint32_t Q[N];
-#pragma unroll
-      for (int i = 0; i < L; ++i) Q[i] = use ? Y[i + 1] : 0u;
-      Q[L] = 0u;
-      Q[L + 1] = 0u;
-      inc_n<N>(Q, use ? inc : 0u);
+      // Q = +-(Y + inc) in N-limb two's complement, one carry chain:
+      // -(Y + inc) = ~Y + (1 - inc)
       const uint32_t neg = (use && t.s != sg) ? 1u : 0u;
       const uint32_t nm = 0u - neg;
+      uint32_t Q[N];
 #pragma unroll
-      for (int i = 0; i < N; ++i) Q[i] ^= nm;
-      inc_n<N>(Q, neg);
+      for (int i = 0; i < L; ++i) Q[i] = (use ? Y[i + 1] : 0u) ^ nm;
+      Q[L] = nm;
+      Q[L + 1] = nm;
+      inc_n<N>(Q, use ? (neg ? 1u - inc : inc) : 0u);
       const int64_t h = hi_of_q<L>(Q);
       int64_t Pi = h;                                 // inclusive scan of h
 #pragma unroll

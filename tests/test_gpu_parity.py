@@ -106,3 +106,54 @@ def test_long_threshold_split_c4(thr, monkeypatch):
     d = gen.make("C4", n=20_000, seed=8)
     for op in ("ax", "atx"):
         assert_same(gpu_run(d, op), oracle_full(d, op), f"C4 threshold {thr} {op}")
+
+
+def _tie_prone_rows(p, nrows, seed):
+    """Rows whose products are engineered against the chain (x = 1, so the
+    products are A's values exactly): grid ties at small gaps, exact
+    cancellation of the running sum, zero entries, binade crossings both ways
+    (the CPU model of the same recipe is tests/test_kernel_algorithms.py)."""
+    import random
+    import oracle
+    rng = random.Random(seed)
+    L = p // 32
+    rowptr, cols, vals = [0], [], []
+    n = 260
+    for _ in range(nrows):
+        ts = []
+        s_e = rng.randint(0, 8)
+        m = rng.choice([8, 33, 64, 100, 250])
+        for k in range(m):
+            kind = rng.random()
+            if kind < 0.25:
+                d = rng.randint(1, 4)
+                M = (1 << (p - 1)) | (1 << (d - 1)) | (rng.getrandbits(p - 1 - d) << d)
+                ts.append((rng.getrandbits(1), M, s_e - d + rng.randint(-1, 1)))
+            elif kind < 0.35:
+                ts.append((0, 0, 0))
+            elif kind < 0.45 and ts:
+                s = oracle.ZERO
+                for t in ts:
+                    s = oracle.add(s, t, p)
+                ts.append((s[0] ^ 1, s[1], s[2]) if s[1] else (0, 1 << (p - 1), s_e))
+            else:
+                ts.append((rng.getrandbits(1), (1 << (p - 1)) | rng.getrandbits(p - 1),
+                           rng.randint(s_e - 6, s_e + 2)))
+        cols += sorted(rng.sample(range(n), m))
+        vals += ts
+        rowptr.append(len(cols))
+    limbs, exps, signs = gen.pack_triples(vals, p)
+    xl, xe, xs = gen.pack_triples([(0, 1 << (p - 1), 1)] * n, p)     # x = 1
+    rp = np.zeros(n + 1, np.int64)
+    rp[1:nrows + 1] = rowptr[1:]
+    rp[nrows + 1:] = rowptr[-1]
+    return dict(p=p, n=n, rowptr=rp, colidx=np.array(cols, np.int32), limbs=limbs, exps=exps,
+                signs=signs, x_limbs=xl, x_exps=xe, x_signs=xs)
+
+
+@pytest.mark.parametrize("thr", ["0", "32"])
+@pytest.mark.parametrize("p", [32, 64, 256, 1024])
+def test_tie_prone_rows(p, thr, monkeypatch):
+    monkeypatch.setenv("MPSP_LONG_T", thr)
+    d = _tie_prone_rows(p, 120, seed=p)
+    assert_same(gpu_run(d, "ax"), oracle_full(d, "ax"), f"tie-prone p={p} T={thr}")

@@ -1,0 +1,250 @@
+"""CPU models of the two non-obvious algorithms inside the CUDA kernels,
+checked against the oracle on adversarial and random inputs.
+
+These are test-side restatements (Python ints) of the REASONING the kernels
+rely on - not of their code - so a flaw in the argument shows up here at CPU
+speed over many more cases than the GPU parity tests run:
+
+1. the short product with an exactness certificate (mp_device.cuh mp_mul):
+   only Comba columns k >= L-3 are formed; if the bits of that partial sum
+   between B = 32(L-2)+5 and the round bit are neither all 0 nor all 1, the
+   rounded product equals RN(a*x) with sticky = 1;
+2. the speculative exact block sum of spmv_wrow.cu: steps of the chain
+   s = RN(s + t_k) whose partial sums provably stay in s's binade are integer
+   additions on the grid u = ulp(s), with ties resolved from the running
+   parity; everything else goes through the exact adder.
+
+Both models are compared bit for bit with oracle.mul / oracle.add chains.
+"""
+import random
+
+import pytest
+
+import oracle
+
+M32 = (1 << 32) - 1
+
+
+# ---------------------------------------------------------------- 1. product
+def short_product(Ma, Mx, p):
+    """Model of mp_mul: returns (M, dE, certified) or None when the
+    certificate fails (the kernel then forms the full product)."""
+    L = p // 32
+    a = [(Ma >> (32 * i)) & M32 for i in range(L)]
+    x = [(Mx >> (32 * i)) & M32 for i in range(L)]
+    K0 = L - 3
+    T = sum(a[i] * x[j] << (32 * (i + j)) for i in range(L) for j in range(L) if i + j >= K0)
+    N = Ma * Mx - T
+    B = 32 * (L - 2) + 5
+    assert 0 <= N < (1 << B)                      # the bound the certificate uses
+    sh = 0 if (T >> (64 * L - 1)) & 1 else 1
+    rpos = 32 * L - 1 - sh                        # round bit position
+    W = (T >> B) & ((1 << (rpos - B)) - 1)
+    if W == 0 or W == (1 << (rpos - B)) - 1:
+        return None
+    q = T >> (rpos + 1)
+    rb = (T >> rpos) & 1
+    q += rb                                       # sticky = 1: round up iff rb
+    dE = -sh
+    if q == 1 << p:
+        q >>= 1
+        dE += 1
+    return q, dE
+
+
+@pytest.mark.parametrize("p", [128, 256, 512, 1024])
+def test_short_product_certificate_random(p):
+    rng = random.Random(p)
+    hits = 0
+    for _ in range(3000):
+        Ma = (1 << (p - 1)) | rng.getrandbits(p - 1)
+        Mx = (1 << (p - 1)) | rng.getrandbits(p - 1)
+        r = short_product(Ma, Mx, p)
+        if r is None:
+            continue
+        hits += 1
+        s, M, E = oracle.mul((0, Ma, 0), (0, Mx, 0), p)
+        assert (M, E) == (r[0], r[1])
+    assert hits == 3000          # random mantissas never need the full product
+
+
+@pytest.mark.parametrize("p", [128, 256, 512])
+def test_short_product_certificate_adversarial(p):
+    """Structured mantissas (powers of two, all-ones runs, carries rippling
+    into the round bit, exact ties): whenever the certificate passes the
+    result is exact; ambiguous cases must be rejected, never mis-rounded."""
+    rng = random.Random(7 * p)
+    top = 1 << (p - 1)
+    corpus = [top, (1 << p) - 1, top | 1, top | (1 << (p // 2)), top + (1 << 32) - 1,
+              (1 << p) - (1 << (p // 2)), top | ((1 << (p // 2)) - 1)]
+    for _ in range(200):
+        corpus.append(top | rng.getrandbits(p - 1))
+        k = rng.randrange(1, p - 1)
+        corpus.append(top | ((1 << k) - 1))             # long runs of ones
+        corpus.append(((1 << p) - 1) ^ (1 << rng.randrange(p - 1)))
+    rejected = 0
+    for Ma in corpus:
+        for Mx in corpus[:60]:
+            r = short_product(Ma, Mx, p)
+            s, M, E = oracle.mul((0, Ma, 0), (0, Mx, 0), p)
+            if r is None:
+                rejected += 1
+                continue
+            assert (M, E) == (r[0], r[1]), (hex(Ma), hex(Mx))
+    assert rejected > 0           # the corpus does exercise the fallback
+
+
+def test_short_product_tie_is_never_certified():
+    """An exact tie has all-zero bits below the round bit: W == 0, so the
+    certificate must reject it (the kernel then rounds the exact product)."""
+    p = 128
+    a = (0, 3 << (p - 2), 2)                 # 3
+    x = (0, (1 << (p - 1)) | 1, 1)           # 1 + 2^-(p-1)
+    assert short_product(a[1], x[1], p) is None
+
+
+# ---------------------------------------------------------------- 2. block sum
+HB = 56
+
+
+def block_sum_chain(ts, p, G=32):
+    """Model of spmv_wrow's chain over the products ts (oracle triples),
+    G steps per block.  Returns (result, n_fast_steps)."""
+    L = p // 32
+    S, E, sg, zero = 0, 0, 0, True         # exact S (grid integer), exponent, sign
+    Shi, err, par = 0, 0, 0
+    nfast = 0
+    H = p - HB                             # log2 of the high-part unit in grid units
+    M1 = 1 if H >= 0 else 1 << (-H)
+
+    def hi(v):                             # floor(v / 2^H) (v may be negative)
+        return v >> H if H >= 0 else v << (-H)
+
+    for b0 in range(0, len(ts), G):
+        blk = ts[b0:b0 + G]
+        start = 0
+        while start < len(blk):
+            if zero:
+                nz = [k for k in range(start, len(blk)) if blk[k][1] != 0]
+                if not nz:
+                    break
+                f = nz[0]
+                sg, S, E = blk[f]
+                zero = False
+                Shi, err, par = hi(S), 1, S & 1
+                start = f + 1
+                continue
+            Q, ties, bad = [], [], []
+            for k in range(len(blk)):
+                st, Mt, Et = blk[k]
+                act = k >= start and Mt != 0
+                if not act:
+                    Q.append(0); ties.append(False); bad.append(False)
+                    continue
+                d = E - Et
+                if d < 1:
+                    Q.append(0); ties.append(False); bad.append(True)
+                    continue
+                d = min(d, 32 * L + 32)
+                Y = Mt >> d
+                rem = Mt & ((1 << d) - 1)
+                half = 1 << (d - 1)
+                tie = rem == half
+                inc = 1 if rem > half else 0
+                Q.append((Y, inc, st != sg))
+                ties.append(tie)
+                bad.append(False)
+            # tie parity, then signed Q, then the conservative checks
+            p_run = par
+            for k in range(len(blk)):
+                if not isinstance(Q[k], tuple):
+                    continue
+                Y, inc, neg = Q[k]
+                if ties[k]:
+                    inc = p_run ^ (Y & 1)
+                    p_run = 0
+                else:
+                    p_run ^= (Y + inc) & 1
+                q = Y + inc
+                Q[k] = -q if neg else q
+            LB, cnt, fail = Shi, 0, None
+            for k in range(len(blk)):
+                h = hi(Q[k])
+                act = k >= start and blk[k][1] != 0
+                if act:
+                    ok = (not bad[k]) and LB + h - M1 >= (1 << (HB - 1)) and \
+                        LB + err + cnt + h + 1 <= (1 << HB)
+                    if not ok:
+                        fail = k
+                        break
+                    cnt += 1
+                LB += h
+            if fail is None:
+                S += sum(Q[start:])
+                Shi, err, par = LB, err + cnt, p_run
+                nfast += cnt
+                assert (1 << (p - 1)) <= S < (1 << p)
+                break
+            S += sum(Q[start:fail])
+            nfast += cnt
+            assert (1 << (p - 1)) <= S < (1 << p)
+            r = oracle.add((sg, S, E), blk[fail], p)
+            sg, S, E = r
+            zero = S == 0
+            Shi, err, par = (hi(S) if not zero else 0), 1, S & 1
+            start = fail + 1
+    return ((0, 0, 0) if zero else (sg, S, E)), nfast
+
+
+def oracle_chain(ts, p):
+    s = oracle.ZERO
+    for t in ts:
+        s = oracle.add(s, t, p)
+    return s
+
+
+def _rand_t(rng, p, elo, ehi):
+    return (rng.getrandbits(1), (1 << (p - 1)) | rng.getrandbits(p - 1), rng.randint(elo, ehi))
+
+
+@pytest.mark.parametrize("p", [32, 64, 256])
+def test_block_sum_random_rows(p):
+    rng = random.Random(p + 1)
+    tot_fast = tot = 0
+    for trial in range(40):
+        n = rng.choice([1, 5, 31, 32, 33, 200, 700])
+        ts = [_rand_t(rng, p, -64, 64) for _ in range(n)]
+        got, nf = block_sum_chain(ts, p)
+        assert got == oracle_chain(ts, p), (trial, n)
+        tot_fast += nf
+        tot += n
+    assert tot_fast > 0.8 * tot        # the fast path carries the long rows
+
+
+@pytest.mark.parametrize("p", [32, 64, 128])
+def test_block_sum_ties_cancellation_and_zeros(p):
+    """Products engineered to tie on the accumulator's grid (d small, low bits
+    10...0), to cancel the accumulator exactly mid-row, zero products, and
+    binade crossings in both directions."""
+    rng = random.Random(3 * p)
+    for trial in range(150):
+        ts = []
+        s_e = rng.randint(0, 8)
+        for k in range(rng.choice([8, 40, 100])):
+            kind = rng.random()
+            if kind < 0.25:        # tie-prone: few low bits set, exponent just below
+                d = rng.randint(1, 4)
+                M = (1 << (p - 1)) | (1 << (d - 1)) | (rng.getrandbits(p - 1 - d) << d)
+                ts.append((rng.getrandbits(1), M, s_e - d + rng.randint(-1, 1)))
+            elif kind < 0.35:
+                ts.append((0, 0, 0))                      # zero product
+            elif kind < 0.45 and ts:
+                prev = oracle_chain(ts, p)                # exact cancellation
+                if prev[1]:
+                    ts.append((prev[0] ^ 1, prev[1], prev[2]))
+                    continue
+                ts.append(_rand_t(rng, p, s_e - 3, s_e + 3))
+            else:
+                ts.append(_rand_t(rng, p, s_e - 6, s_e + 2))
+        got, _ = block_sum_chain(ts, p, G=rng.choice([4, 32]))
+        assert got == oracle_chain(ts, p), trial
