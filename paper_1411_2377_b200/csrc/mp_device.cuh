@@ -334,27 +334,48 @@ __device__ __forceinline__ uint32_t clz_limbs(const uint32_t (&v)[N]) {
   return lz;
 }
 
+// z = x + y + cin (N limbs, cin in {0,1}); returns the carry out
+template <int N>
+__device__ __forceinline__ uint32_t add_n_cin(uint32_t (&z)[N], const uint32_t (&x)[N],
+                                              const uint32_t (&y)[N], uint32_t cin) {
+  uint32_t c, dummy;
+  asm volatile("add.cc.u32 %0, %1, 0xffffffff;" : "=r"(dummy) : "r"(cin));  // CF = cin
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+    asm volatile("addc.cc.u32 %0, %1, %2;" : "=r"(z[i]) : "r"(x[i]), "r"(y[i]));
+  asm volatile("addc.u32 %0, 0, 0;" : "=r"(c));
+  return c;
+}
+
 // --------------------------------------------------------------------------
 // s = RN_p(s + t)   (the oracle's add() computes the
 // same value by exact integer alignment).  Working width: L+1 limbs, i.e.
 // one 32-bit guard limb below the LSB, plus a sticky word for bits shifted
 // beyond it.  |exponent gap| >= p+2 returns the larger operand (far-path
 // lemma).
+//
+// ONE branch-free path for every case (no near/far split: in a warp of
+// independent rows the two paths diverge in most steps, and both would run):
+//   Z = big * 2^32, Y = small * 2^32 >> d  (sticky: bits beyond the guard);
+//   Z := Z + (Y ^ m) + cin,  m = cin = 0 for equal signs, m = ~0 and
+//        cin = 1 - [sticky] for opposite signs (Z - Y - [sticky]; exact for
+//        d <= 1, where nothing reaches the sticky);
+//   equal signs: shift right by the carry W (the dropped bit joins the sticky);
+//   then shift left by lz = clz(top limb) (0 or 1 for d >= 2; any amount for
+//   the cancellation at d <= 1; >= 32 bits of cancellation or an exact zero
+//   take the one rare branch);  e = e_big + W - lz;  round to nearest even.
 // --------------------------------------------------------------------------
 template <int L>
 __device__ __forceinline__ void mp_add(MP<L>& s, const MP<L>& t) {
-  // Branch-free zero handling: a zero operand becomes the "small" operand
-  // with d = 0 and contributes nothing; both zero gives a zero mantissa.
   const bool tz = t.is_zero(), sz = s.is_zero();
   const uint32_t mlt = lt_n<L>(s.m, t.m);               // |M_s| < |M_t|
   const bool t_big = !tz && (sz || t.e > s.e || (t.e == s.e && mlt));
   const int32_t eb = t_big ? t.e : s.e;
   const int32_t esm = t_big ? s.e : t.e;
   const uint32_t sb = t_big ? t.s : s.s;
-  const bool same = (t.s == s.s);
+  const uint32_t sub = (t.s != s.s && !tz && !sz) ? 1u : 0u;
   uint32_t d = (uint32_t)eb - (uint32_t)esm;            // exact as uint32
   d = (tz || sz) ? 0u : min(d, (uint32_t)(32 * (L + 1)));  // d >= p+2: all sticky
-  // Z = big * 2^32 (guard limb Z[0]); Y = small * 2^32, to be aligned
   uint32_t Z[L + 1], Y[L + 1];
   Z[0] = 0u;
   Y[0] = 0u;
@@ -363,43 +384,27 @@ __device__ __forceinline__ void mp_add(MP<L>& s, const MP<L>& t) {
     Z[i + 1] = t_big ? t.m[i] : s.m[i];
     Y[i + 1] = t_big ? s.m[i] : t.m[i];
   }
-  int32_t e;
   uint32_t stk = 0u;
-  if (!same && d <= 1u) {
-    // ---- near path: exact subtraction, then normalise left by lz
+  shr_bits_sticky<L + 1>(Y, d, stk);
+  const uint32_t msk = 0u - sub;
 #pragma unroll
-    for (int i = 0; i < L; ++i) Y[i] = __funnelshift_r(Y[i], Y[i + 1], d);
-    Y[L] >>= d;
-    sub_n<L + 1>(Z, Z, Y, 0u);
-    uint32_t lz = __clz(Z[L]);
-    if (lz < 32u) {
+  for (int i = 0; i <= L; ++i) Y[i] ^= msk;
+  const uint32_t cin = sub & (stk == 0u ? 1u : 0u);
+  const uint32_t W = add_n_cin<L + 1>(Z, Z, Y, cin) & (sub ^ 1u);
+  stk |= Z[0] & W;                                      // bit lost by the right shift
 #pragma unroll
-      for (int i = L; i > 0; --i) Z[i] = __funnelshift_l(Z[i - 1], Z[i], lz);
-      Z[0] <<= lz;
-    } else {            // >= 32 bits cancelled, or exact zero (rare)
-      lz = clz_limbs<L + 1>(Z);
-      shl_bits<L + 1>(Z, lz);
-    }
-    e = eb - (int32_t)lz;
-  } else {
-    // ---- far path (d >= 2, or same sign): align small, add/sub, <= 1-bit norm
-    shr_bits_sticky<L + 1>(Y, d, stk);
-    if (same) {
-      const uint32_t c = add_n<L + 1>(Z, Z, Y);
-      stk |= Z[0] & c;                                   // bit lost by the 1-bit shift
+  for (int i = 0; i < L; ++i) Z[i] = __funnelshift_r(Z[i], Z[i + 1], W);
+  Z[L] = __funnelshift_r(Z[L], W, W);
+  uint32_t lz = __clz(Z[L]);
+  if (lz < 32u) {
 #pragma unroll
-      for (int i = 0; i < L; ++i) Z[i] = __funnelshift_r(Z[i], Z[i + 1], c);
-      Z[L] = __funnelshift_r(Z[L], c, c);
-      e = eb + (int32_t)c;
-    } else {
-      sub_n<L + 1>(Z, Z, Y, stk != 0u ? 1u : 0u);       // X - Y - [sticky]
-      const uint32_t sh = (~Z[L]) >> 31;                // top bit clear -> shift 1
-#pragma unroll
-      for (int i = L; i > 0; --i) Z[i] = __funnelshift_l(Z[i - 1], Z[i], sh);
-      Z[0] <<= sh;
-      e = eb - (int32_t)sh;
-    }
+    for (int i = L; i > 0; --i) Z[i] = __funnelshift_l(Z[i - 1], Z[i], lz);
+    Z[0] <<= lz;
+  } else {            // >= 32 bits cancelled, or an exact zero (rare)
+    lz = clz_limbs<L + 1>(Z);
+    shl_bits<L + 1>(Z, lz);
   }
+  const int32_t e = eb + (int32_t)W - (int32_t)lz;
   const uint32_t rb = Z[0] >> 31;
   const uint32_t st = stk | (Z[0] << 1);
 #pragma unroll
