@@ -34,8 +34,10 @@ struct PartView {
   const uint32_t* limbs;      // [nentries * L]
   int64_t nslots;             // 32 * nslices (SELL part: short rows)
   int64_t nslices;
-  // warp rows (rows longer than the long-row threshold), longest first
+  // warp rows (rows longer than the long-row threshold), longest first;
+  // the first npcrow of them (length >= the pc threshold) go to spmv_pcrow
   int64_t nwrow;
+  int64_t npcrow;
   const int64_t* wrow_ptr;    // [nwrow] first entry (multiple of 32)
   const int32_t* wrow_row;    // [nwrow] output row (local)
   const int32_t* wrow_len;    // [nwrow]
@@ -59,6 +61,10 @@ int launch_spmv(int L, const PartView& P, const XView& x, const YView& y, void* 
 int launch_spmv_long(int L, const PartView& P, const XView& x, const YView& y, void* stream);
 // Row-length threshold above which a row goes to the warp-row kernel.
 int long_row_threshold();
+// Row-length threshold from which a warp row goes to spmv_pcrow.
+int pc_row_threshold();
+// Producer/consumer kernel over warp rows [0, P.npcrow); cudaError_t value.
+int launch_spmv_pc(int L, const PartView& P, const XView& x, const YView& y, void* stream);
 // Launch counter increment (shared by the kernel files).
 void launch_counter_add(int64_t k);
 // Integer-MAC microbenchmark (roofline denominator); returns cudaError_t.

@@ -40,6 +40,13 @@ int long_row_threshold() {
   return v ? std::atoi(v) : 128;
 }
 
+// Rows at least this long (and above the warp-row threshold) go to the
+// producer/consumer kernel spmv_pcrow (tests lower it to route rows there).
+int pc_row_threshold() {
+  const char* v = std::getenv("MPSP_PC_T");
+  return v ? std::atoi(v) : 1024;
+}
+
 // High-part scale H: S/H in [2^(HB-1), 2^HB).  HB = 56 keeps a 32-lane scan
 // of |h| <= 2^55 far from int64 overflow.
 constexpr int HB = 56;
@@ -113,54 +120,57 @@ __device__ __forceinline__ int wcol(const PartView& P, int64_t e0, int jb, int l
   return (jb + lane < len) ? __ldg(P.col + e0 + jb + lane) : 0;
 }
 
+// The chain state of one row held by one warp, and the exact block sum.
 template <int L>
-__global__ void __launch_bounds__(128) spmv_wrow(PartView P, XView x, YView y) {
-  constexpr int N = L + 2;
-  constexpr unsigned FULL = 0xffffffffu;
-  constexpr int64_t LO = (int64_t)1 << (HB - 1), HI = (int64_t)1 << HB;
-  constexpr int64_t M1 = (L == 1) ? ((int64_t)1 << (HB - 32)) : 1;   // one grid unit u, in H
-  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= P.nwrow) return;
-  const int64_t e0 = P.wrow_ptr[w];
-  const int len = P.wrow_len[w];
-  const int row = P.wrow_row[w];
-  const unsigned below = (1u << lane) - 1u;
+struct WChain {
+  static constexpr int N = L + 2;
+  uint32_t R[N];          // this lane's share of S (two's complement)
+  bool szero;             // accumulator is exactly zero (warp-uniform)
+  int32_t E;              // accumulator exponent (warp-uniform)
+  uint32_t sg;            // accumulator sign
+  int64_t Shi, err;       // S/H in [Shi, Shi + err)
+  uint32_t par;           // parity of S
 
-  uint32_t R[N];                      // this lane's share of S (two's complement)
+  __device__ __forceinline__ void init() {
 #pragma unroll
-  for (int i = 0; i < N; ++i) R[i] = 0u;
-  bool szero = true;                  // accumulator is exactly zero (warp-uniform)
-  int32_t E = 0;                      // accumulator exponent (warp-uniform)
-  uint32_t sg = 0u;                   // accumulator sign
-  int64_t Shi = 0, err = 0;           // S/H in [Shi, Shi + err)
-  uint32_t par = 0u;                  // parity of S
-
-  WEntry<L> nxt;
-  int cnext = 0;                      // columns of the block after the prefetched one
-  if (WPrefetch<L>::on) {
-    wload<L>(P, x, e0, 0, len, lane, wcol(P, e0, 0, len, lane), nxt);
-    cnext = wcol(P, e0, 32, len, lane);
-  } else {
-    cnext = wcol(P, e0, 0, len, lane);
+    for (int i = 0; i < N; ++i) R[i] = 0u;
+    szero = true;
+    E = 0;
+    sg = 0u;
+    Shi = 0;
+    err = 0;
+    par = 0u;
   }
-  for (int jb = 0; jb < len; jb += 32) {
-    MP<L> t;
-    {
-      WEntry<L> cur;
-      if constexpr (WPrefetch<L>::on) {
-        cur = nxt;
-        if (jb + 32 < len) {
-          wload<L>(P, x, e0, jb + 32, len, lane, cnext, nxt);
-          cnext = wcol(P, e0, jb + 64, len, lane);
-        }
-      } else {
-        wload<L>(P, x, e0, jb, len, lane, cnext, cur);
-        cnext = wcol(P, e0, jb + 32, len, lane);
-      }
-      const int32_t ea = (int32_t)((uint32_t)cur.w << 1) >> 1;
-      mp_mul<L>(cur.a, ea, (uint32_t)cur.w >> 31, cur.x, cur.ex, cur.sx, t);
-    }
+
+  __device__ __forceinline__ void reset_to(const MP<L>& s, int lane) {
+    szero = s.is_zero();
+#pragma unroll
+    for (int i = 0; i < N; ++i) R[i] = (lane == 0 && i < L) ? s.m[i] : 0u;
+    E = s.e;
+    sg = s.s;
+    Shi = szero ? 0 : hi_of_mant<L>(s.m);
+    err = 1;
+    par = s.m[0] & 1u;
+  }
+
+  // exact S (all lanes)
+  __device__ __forceinline__ void exact(MP<L>& s) const {
+    uint32_t S[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) S[i] = R[i];
+    warp_sum_limbs<N>(S);
+#pragma unroll
+    for (int i = 0; i < L; ++i) s.m[i] = szero ? 0u : S[i];
+    s.e = E;
+    s.s = sg;
+  }
+
+  // s := the chain over this warp's 32 products t (lane k holds step k)
+  __device__ __forceinline__ void consume(const MP<L>& t, int lane) {
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int64_t LO = (int64_t)1 << (HB - 1), HI = (int64_t)1 << HB;
+    constexpr int64_t M1 = (L == 1) ? ((int64_t)1 << (HB - 32)) : 1;   // grid unit u, in H
+    const unsigned below = (1u << lane) - 1u;
     const bool tz = t.is_zero();       // padding lanes have zero limbs
     int start = 0;
     while (start < 32) {
@@ -169,17 +179,12 @@ __global__ void __launch_bounds__(128) spmv_wrow(PartView P, XView x, YView y) {
         const unsigned nzm = __ballot_sync(FULL, !tz && lane >= start);
         if (nzm == 0u) break;
         const int f = __ffs(nzm) - 1;
-        uint32_t m[L];
+        MP<L> tf;
 #pragma unroll
-        for (int i = 0; i < L; ++i) m[i] = __shfl_sync(FULL, t.m[i], f);
-        E = __shfl_sync(FULL, t.e, f);
-        sg = __shfl_sync(FULL, t.s, f);
-#pragma unroll
-        for (int i = 0; i < N; ++i) R[i] = (lane == 0 && i < L) ? m[i] : 0u;
-        Shi = hi_of_mant<L>(m);
-        err = 1;
-        par = m[0] & 1u;
-        szero = false;
+        for (int i = 0; i < L; ++i) tf.m[i] = __shfl_sync(FULL, t.m[i], f);
+        tf.e = __shfl_sync(FULL, t.e, f);
+        tf.s = __shfl_sync(FULL, t.s, f);
+        reset_to(tf, lane);
         start = f + 1;
         continue;
       }
@@ -245,52 +250,150 @@ __global__ void __launch_bounds__(128) spmv_wrow(PartView P, XView x, YView y) {
       // ---- exact path at the first failing step f
       const int f = __ffs(failM) - 1;
       if (lane < f) add_n<N>(R, R, Q);               // steps before f are valid
-      uint32_t S[N];
-#pragma unroll
-      for (int i = 0; i < N; ++i) S[i] = R[i];
-      warp_sum_limbs<N>(S);
       MP<L> s, tf;
+      exact(s);
 #pragma unroll
-      for (int i = 0; i < L; ++i) {
-        s.m[i] = S[i];
-        tf.m[i] = __shfl_sync(FULL, t.m[i], f);
-      }
-      s.e = E;
-      s.s = sg;
+      for (int i = 0; i < L; ++i) tf.m[i] = __shfl_sync(FULL, t.m[i], f);
       tf.e = __shfl_sync(FULL, t.e, f);
       tf.s = __shfl_sync(FULL, t.s, f);
       mp_add<L>(s, tf);
-      szero = s.is_zero();
-#pragma unroll
-      for (int i = 0; i < N; ++i) R[i] = (lane == 0 && i < L) ? s.m[i] : 0u;
-      E = s.e;
-      sg = s.s;
-      Shi = szero ? 0 : hi_of_mant<L>(s.m);
-      err = 1;
-      par = s.m[0] & 1u;
+      reset_to(s, lane);
       start = f + 1;
     }
   }
-  MP<L> s;
-  {
-    uint32_t S[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) S[i] = R[i];
-    warp_sum_limbs<N>(S);
-#pragma unroll
-    for (int i = 0; i < L; ++i) s.m[i] = szero ? 0u : S[i];
+};
+
+template <int L>
+__global__ void __launch_bounds__(128) spmv_wrow(PartView P, XView x, YView y) {
+  const int64_t w = P.npcrow + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= P.nwrow) return;
+  const int64_t e0 = P.wrow_ptr[w];
+  const int len = P.wrow_len[w];
+  const int row = P.wrow_row[w];
+  WChain<L> ch;
+  ch.init();
+
+  WEntry<L> nxt;
+  int cnext = 0;                      // columns of the block after the prefetched one
+  if (WPrefetch<L>::on) {
+    wload<L>(P, x, e0, 0, len, lane, wcol(P, e0, 0, len, lane), nxt);
+    cnext = wcol(P, e0, 32, len, lane);
+  } else {
+    cnext = wcol(P, e0, 0, len, lane);
   }
-  s.e = E;
-  s.s = sg;
+  for (int jb = 0; jb < len; jb += 32) {
+    MP<L> t;
+    {
+      WEntry<L> cur;
+      if constexpr (WPrefetch<L>::on) {
+        cur = nxt;
+        if (jb + 32 < len) {
+          wload<L>(P, x, e0, jb + 32, len, lane, cnext, nxt);
+          cnext = wcol(P, e0, jb + 64, len, lane);
+        }
+      } else {
+        wload<L>(P, x, e0, jb, len, lane, cnext, cur);
+        cnext = wcol(P, e0, jb + 32, len, lane);
+      }
+      const int32_t ea = (int32_t)((uint32_t)cur.w << 1) >> 1;
+      mp_mul<L>(cur.a, ea, (uint32_t)cur.w >> 31, cur.x, cur.ex, cur.sx, t);
+    }
+    ch.consume(t, lane);
+  }
+  MP<L> s;
+  ch.exact(s);
+  if (lane == 0 && row >= 0) store_y<L>(y, row, s);
+}
+
+// --------------------------------------------------------------------------
+// spmv_pcrow<L>: the longest rows, one CTA per row.  Warp 0 runs the chain
+// (WChain::consume, 32 steps per block); warps 1..PCP compute the products
+// (block b by producer b % PCP) into a double-buffered shared-memory slot
+// per producer, handed over with named barriers (FULL: producer -> chain,
+// EMPTY: chain -> producer).  The chain warp then only pays the block sum,
+// so a 5000-long row's critical path is ~157 block sums.
+// --------------------------------------------------------------------------
+constexpr int PCP = 3;                               // producer warps
+constexpr int PC_THREADS = 32 * (PCP + 1);
+
+__device__ __forceinline__ void bar_sync_n(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive_n(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int L>
+__global__ void __launch_bounds__(PC_THREADS) spmv_pcrow(PartView P, XView x, YView y) {
+  constexpr int SW = L + 2;                          // words per product
+  __shared__ uint32_t slot[PCP][2][SW][32];          // [producer][buffer][word][lane]
+  const int64_t w = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t e0 = P.wrow_ptr[w];
+  const int len = P.wrow_len[w];
+  const int nblk = (len + 31) / 32;
+  if (warp > 0) {
+    const int p = warp - 1;
+    WEntry<L> nxt;
+    int cnext = 0;
+    if (p < nblk) {
+      wload<L>(P, x, e0, 32 * p, len, lane, wcol(P, e0, 32 * p, len, lane), nxt);
+      cnext = wcol(P, e0, 32 * (p + PCP), len, lane);
+    }
+    for (int b = p, i = 0; b < nblk; b += PCP, ++i) {
+      const int j = i & 1;
+      WEntry<L> cur = nxt;
+      if (b + PCP < nblk) {
+        wload<L>(P, x, e0, 32 * (b + PCP), len, lane, cnext, nxt);
+        cnext = wcol(P, e0, 32 * (b + 2 * PCP), len, lane);
+      }
+      MP<L> t;
+      const int32_t ea = (int32_t)((uint32_t)cur.w << 1) >> 1;
+      mp_mul<L>(cur.a, ea, (uint32_t)cur.w >> 31, cur.x, cur.ex, cur.sx, t);
+      if (i >= 2) bar_sync_n(1 + PCP * 2 + 2 * p + j, 64);      // EMPTY(p, j)
+#pragma unroll
+      for (int k = 0; k < L; ++k) slot[p][j][k][lane] = t.m[k];
+      slot[p][j][L][lane] = (uint32_t)t.e;
+      slot[p][j][L + 1][lane] = t.s;
+      bar_arrive_n(1 + 2 * p + j, 64);                           // FULL(p, j)
+    }
+    return;
+  }
+  WChain<L> ch;
+  ch.init();
+  for (int b = 0; b < nblk; ++b) {
+    const int p = b % PCP, i = b / PCP, j = i & 1;
+    bar_sync_n(1 + 2 * p + j, 64);                               // FULL(p, j)
+    MP<L> t;
+#pragma unroll
+    for (int k = 0; k < L; ++k) t.m[k] = slot[p][j][k][lane];
+    t.e = (int32_t)slot[p][j][L][lane];
+    t.s = slot[p][j][L + 1][lane];
+    if (b + 2 * PCP < nblk) bar_arrive_n(1 + PCP * 2 + 2 * p + j, 64);   // EMPTY(p, j)
+    ch.consume(t, lane);
+  }
+  MP<L> s;
+  ch.exact(s);
+  const int row = P.wrow_row[w];
   if (lane == 0 && row >= 0) store_y<L>(y, row, s);
 }
 
 template <int L>
 static int launch_wrow_L(const PartView& P, const XView& x, const YView& y, cudaStream_t st) {
-  if (P.nwrow <= 0) return 0;
+  const int64_t nw = P.nwrow - P.npcrow;
+  if (nw <= 0) return 0;
   const int threads = 128;
-  const int64_t blocks = (P.nwrow * 32 + threads - 1) / threads;
+  const int64_t blocks = (nw * 32 + threads - 1) / threads;
   spmv_wrow<L><<<(unsigned)blocks, threads, 0, st>>>(P, x, y);
+  launch_counter_add(1);
+  return (int)cudaGetLastError();
+}
+
+template <int L>
+static int launch_pcrow_L(const PartView& P, const XView& x, const YView& y, cudaStream_t st) {
+  if (P.npcrow <= 0) return 0;
+  spmv_pcrow<L><<<(unsigned)P.npcrow, PC_THREADS, 0, st>>>(P, x, y);
   launch_counter_add(1);
   return (int)cudaGetLastError();
 }
@@ -304,6 +407,19 @@ int launch_spmv_long(int L, const PartView& P, const XView& x, const YView& y, v
     case 8: return launch_wrow_L<8>(P, x, y, st);
     case 16: return launch_wrow_L<16>(P, x, y, st);
     case 32: return launch_wrow_L<32>(P, x, y, st);
+    default: return (int)cudaErrorInvalidValue;
+  }
+}
+
+int launch_spmv_pc(int L, const PartView& P, const XView& x, const YView& y, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (L) {
+    case 1: return launch_pcrow_L<1>(P, x, y, st);
+    case 2: return launch_pcrow_L<2>(P, x, y, st);
+    case 4: return launch_pcrow_L<4>(P, x, y, st);
+    case 8: return launch_pcrow_L<8>(P, x, y, st);
+    case 16: return launch_pcrow_L<16>(P, x, y, st);
+    case 32: return launch_pcrow_L<32>(P, x, y, st);
     default: return (int)cudaErrorInvalidValue;
   }
 }

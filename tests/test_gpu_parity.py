@@ -157,3 +157,31 @@ def test_tie_prone_rows(p, thr, monkeypatch):
     monkeypatch.setenv("MPSP_LONG_T", thr)
     d = _tie_prone_rows(p, 120, seed=p)
     assert_same(gpu_run(d, "ax"), oracle_full(d, "ax"), f"tie-prone p={p} T={thr}")
+
+
+@pytest.fixture
+def all_rows_pc(monkeypatch):
+    """Route every nonempty row through the producer/consumer kernel."""
+    monkeypatch.setenv("MPSP_LONG_T", "0")
+    monkeypatch.setenv("MPSP_PC_T", "1")
+
+
+@pytest.mark.parametrize("p", PS)
+def test_pc_kernel_stress(p, all_rows_pc):
+    d = gen.stress(p, seed=9)
+    for op in ("ax", "atx"):
+        assert_same(gpu_run(d, op), oracle_full(d, op), f"pc-kernel stress p={p} {op}")
+
+
+@pytest.mark.parametrize("p", [32, 256, 1024])
+def test_pc_kernel_tie_prone(p, all_rows_pc):
+    d = _tie_prone_rows(p, 60, seed=p + 5)
+    assert_same(gpu_run(d, "ax"), oracle_full(d, "ax"), f"pc tie-prone p={p}")
+
+
+@pytest.mark.parametrize("pc", ["100", "300"])
+def test_pc_threshold_split_c4(pc, monkeypatch):
+    monkeypatch.setenv("MPSP_PC_T", pc)
+    d = gen.make("C4", n=20_000, seed=10)
+    for op in ("ax", "atx"):
+        assert_same(gpu_run(d, op), oracle_full(d, op), f"C4 pc threshold {pc} {op}")
