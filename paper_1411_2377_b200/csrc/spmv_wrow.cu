@@ -26,6 +26,7 @@
 // binade.  Nothing is approximated: the bounds only decide fast vs exact.
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdint>
 #include <cstdlib>
 
@@ -44,33 +45,23 @@ int long_row_threshold() {
 // producer/consumer kernel spmv_pcrow (tests lower it to route rows there).
 int pc_row_threshold() {
   const char* v = std::getenv("MPSP_PC_T");
-  return v ? std::atoi(v) : 1024;
+  return v ? std::atoi(v) : INT_MAX;                 // opt-in (no faster yet)
 }
 
-// High-part scale H: S/H in [2^(HB-1), 2^HB).  HB = 56 keeps a 32-lane scan
-// of |h| <= 2^55 far from int64 overflow.
-constexpr int HB = 56;
+// High-part scale H = 2^(p-HB) grid units: S/H in [2^(HB-1), 2^HB).  HB = 26
+// keeps the 32-lane scan of |h| <= 2^25 (plus Shi and the error count) in
+// int32; one unit of H is >= one grid unit u for every p >= 32.
+constexpr int HB = 26;
 
 template <int L>
-__device__ __forceinline__ int64_t hi_of_mant(const uint32_t (&m)[L]) {
-  if constexpr (L == 1) {
-    return (int64_t)m[0] << (HB - 32);
-  } else {
-    return (int64_t)((((uint64_t)m[L - 1] << 32) | m[L - 2]) >> (64 - HB));
-  }
+__device__ __forceinline__ int32_t hi_of_mant(const uint32_t (&m)[L]) {
+  return (int32_t)(m[L - 1] >> (32 - HB));
 }
 
 // floor(Q / H) for an (L+2)-limb two's complement Q with |Q| <= 2^(p-1) + 1
 template <int L>
-__device__ __forceinline__ int64_t hi_of_q(const uint32_t (&Q)[L + 2]) {
-  if constexpr (L == 1) {
-    const int64_t v = (int64_t)(((uint64_t)Q[1] << 32) | Q[0]);
-    return v * ((int64_t)1 << (HB - 32));
-  } else {
-    const uint32_t lo = __funnelshift_r(Q[L - 2], Q[L - 1], 64 - HB);
-    const uint32_t hi = __funnelshift_r(Q[L - 1], Q[L], 64 - HB);
-    return (int64_t)(((uint64_t)hi << 32) | lo);
-  }
+__device__ __forceinline__ int32_t hi_of_q(const uint32_t (&Q)[L + 2]) {
+  return (int32_t)__funnelshift_r(Q[L - 1], Q[L], 32 - HB);
 }
 
 template <int N>
@@ -128,8 +119,7 @@ struct WChain {
   bool szero;             // accumulator is exactly zero (warp-uniform)
   int32_t E;              // accumulator exponent (warp-uniform)
   uint32_t sg;            // accumulator sign
-  int64_t Shi, err;       // S/H in [Shi, Shi + err)
-  uint32_t par;           // parity of S
+  int32_t Shi, err;       // S/H in [Shi, Shi + err)
 
   __device__ __forceinline__ void init() {
 #pragma unroll
@@ -139,7 +129,6 @@ struct WChain {
     sg = 0u;
     Shi = 0;
     err = 0;
-    par = 0u;
   }
 
   __device__ __forceinline__ void reset_to(const MP<L>& s, int lane) {
@@ -150,7 +139,6 @@ struct WChain {
     sg = s.s;
     Shi = szero ? 0 : hi_of_mant<L>(s.m);
     err = 1;
-    par = s.m[0] & 1u;
   }
 
   // exact S (all lanes)
@@ -168,8 +156,7 @@ struct WChain {
   // s := the chain over this warp's 32 products t (lane k holds step k)
   __device__ __forceinline__ void consume(const MP<L>& t, int lane) {
     constexpr unsigned FULL = 0xffffffffu;
-    constexpr int64_t LO = (int64_t)1 << (HB - 1), HI = (int64_t)1 << HB;
-    constexpr int64_t M1 = (L == 1) ? ((int64_t)1 << (HB - 32)) : 1;   // grid unit u, in H
+    constexpr int32_t LO = 1 << (HB - 1), HI = 1 << HB;
     const unsigned below = (1u << lane) - 1u;
     const bool tz = t.is_zero();       // padding lanes have zero limbs
     int start = 0;
@@ -205,17 +192,19 @@ struct WChain {
       const bool tie = use && rb && !sticky;
       uint32_t inc = (rb && sticky) ? 1u : 0u;
       const uint32_t lsbY = Y[1] & 1u;
-      const unsigned actM = __ballot_sync(FULL, act);
       const unsigned tieM = __ballot_sync(FULL, tie);
-      const unsigned bM = __ballot_sync(FULL, use && !tie && ((lsbY ^ inc) & 1u));
-      if (tie) {
-        // parity of S_{k-1}: reset to 0 by the last tie before k, then the
-        // XOR of the non-tie Q_j low bits since
-        const unsigned tb = tieM & below;
-        const int lt = tb ? 31 - __clz(tb) : -1;
-        const unsigned seg = below & (lt >= 0 ? ~((2u << lt) - 1u) : FULL);
-        const uint32_t pS = ((lt >= 0 ? 0u : par) ^ (uint32_t)__popc(bM & seg)) & 1u;
-        inc = pS ^ lsbY;                              // make S_k even
+      if (tieM) {                                     // warp-uniform, rare
+        // parity of S_{k-1}: that of S (XOR of the lanes' R low bits), reset
+        // to 0 by the last tie before k, XORed with the non-tie Q_j low bits
+        const uint32_t par = (uint32_t)__popc(__ballot_sync(FULL, R[0] & 1u)) & 1u;
+        const unsigned bM = __ballot_sync(FULL, use && !tie && ((lsbY ^ inc) & 1u));
+        if (tie) {
+          const unsigned tb = tieM & below;
+          const int lt = tb ? 31 - __clz(tb) : -1;
+          const unsigned seg = below & (lt >= 0 ? ~((2u << lt) - 1u) : FULL);
+          const uint32_t pS = ((lt >= 0 ? 0u : par) ^ (uint32_t)__popc(bM & seg)) & 1u;
+          inc = pS ^ lsbY;                            // make S_k even
+        }
       }
       // Q = +-(Y + inc) in N-limb two's complement, one carry chain:
       // -(Y + inc) = ~Y + (1 - inc)
@@ -227,24 +216,21 @@ struct WChain {
       Q[L] = nm;
       Q[L + 1] = nm;
       inc_n<N>(Q, use ? (neg ? 1u - inc : inc) : 0u);
-      const int64_t h = hi_of_q<L>(Q);
-      int64_t Pi = h;                                 // inclusive scan of h
+      const int32_t h = hi_of_q<L>(Q);
+      int32_t Pi = h;                                 // inclusive scan of h
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int64_t v = __shfl_up_sync(FULL, Pi, o);
+        const int32_t v = __shfl_up_sync(FULL, Pi, o);
         if (lane >= o) Pi += v;
       }
-      const int64_t LB = Shi + (Pi - h);              // S_{k-1}/H >= LB
-      const int64_t ek = err + __popc(actM & below);  // S_{k-1}/H < LB + ek
-      const bool ok = !act || (!badd && LB + h - M1 >= LO && LB + ek + h + 1 <= HI);
+      const int32_t LB = Shi + (Pi - h);              // S_{k-1}/H >= LB
+      const int32_t ek = err + lane;                  // S_{k-1}/H < LB + ek
+      const bool ok = !act || (!badd && LB + h - 1 >= LO && LB + ek + h + 1 <= HI);
       const unsigned failM = __ballot_sync(FULL, !ok);
       if (failM == 0u) {
         add_n<N>(R, R, Q);
         Shi += __shfl_sync(FULL, Pi, 31);
-        err += __popc(actM);
-        const int lt = tieM ? 31 - __clz(tieM) : -1;
-        const unsigned seg = lt >= 0 ? ~((2u << lt) - 1u) : FULL;
-        par = ((lt >= 0 ? 0u : par) ^ (uint32_t)__popc(bM & seg)) & 1u;
+        err = min(err + 32, 1 << 28);                 // saturates: checks then fail
         break;
       }
       // ---- exact path at the first failing step f

@@ -104,7 +104,7 @@ def test_short_product_tie_is_never_certified():
 
 
 # ---------------------------------------------------------------- 2. block sum
-HB = 56
+HB = 26
 
 
 def block_sum_chain(ts, p, G=32):
@@ -115,7 +115,7 @@ def block_sum_chain(ts, p, G=32):
     Shi, err, par = 0, 0, 0
     nfast = 0
     H = p - HB                             # log2 of the high-part unit in grid units
-    M1 = 1 if H >= 0 else 1 << (-H)
+    M1 = 1                                 # one grid unit u <= one H unit (p >= HB)
 
     def hi(v):                             # floor(v / 2^H) (v may be negative)
         return v >> H if H >= 0 else v << (-H)
@@ -172,8 +172,9 @@ def block_sum_chain(ts, p, G=32):
                 h = hi(Q[k])
                 act = k >= start and blk[k][1] != 0
                 if act:
+                    # the kernel bounds the floor errors before step k by k
                     ok = (not bad[k]) and LB + h - M1 >= (1 << (HB - 1)) and \
-                        LB + err + cnt + h + 1 <= (1 << HB)
+                        LB + err + k + h + 1 <= (1 << HB)
                     if not ok:
                         fail = k
                         break
@@ -181,7 +182,7 @@ def block_sum_chain(ts, p, G=32):
                 LB += h
             if fail is None:
                 S += sum(Q[start:])
-                Shi, err, par = LB, err + cnt, p_run
+                Shi, err, par = LB, min(err + G, 1 << 28), p_run
                 nfast += cnt
                 assert (1 << (p - 1)) <= S < (1 << p)
                 break
