@@ -338,8 +338,19 @@ def main():
         roof = {"bound": "hbm", "achieved": bytes_local / kern_avg_s / 1e9, "peak": hbm_peak,
                 "unit": "GB/s", "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    # DRAM bytes per launch of the dominant kernel from the committed ncu
+    # --set full capture of this workload (tools/traffic_from_ncu.py)
     roof["traffic"] = None
-    roof["kernel"] = f"spmv_sell<{L}>"
+    tj = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tj) and world == 1:
+        rec = json.load(open(tj)).get(f"{args.config} {args.op}")
+        if rec:
+            roof["traffic"] = rec["traffic_bytes"]
+            roof["traffic_source"] = f"profiles/{rec['summary'] or rec['report']} ({rec['kernel']})"
+            roof["algorithmic_bytes"] = bytes_local
+    thr = int(os.environ.get("MPSP_LONG_T", "128"))
+    roof["kernel"] = (f"spmv_sell<{L}>" if d["meta"]["max_row"] <= thr or args.op == "atx" else
+                      f"spmv_sell<{L}> + spmv_wrow<{L}> (concurrent streams, fork/join timed as one)")
     roof["kernel_ms"] = kern_avg_s * 1e3
     roof["t_roof_ms"] = max(t_mem, t_int) * 1e3
     roof["frac_of_t_roof"] = max(t_mem, t_int) / kern_avg_s

@@ -58,28 +58,41 @@ __global__ void __launch_bounds__(128, MINB) spmv_sell(PartView P, XView x, YVie
     mp_mul<L>(a, ea, (uint32_t)w >> 31, xv, ex, sx, t);
     mp_add<L>(s, t);
   };
-  int cnext = 0;                          // column of the next entry to fetch
+  // columns run two entries ahead of the fetches that use them (c1: entry
+  // j+1, c2: entry j+2 at the top of iteration j): a column load from HBM
+  // takes longer than one step
+  int c1 = 0, c2 = 0;
   if (len > 0) {
     fetch(0, __ldg(colp), a0, x0, w0, e0, s0);
-    if (len > 1) cnext = __ldg(colp + 32);
+    if (len > 1) c1 = __ldg(colp + 32);
+    if (len > 2) c2 = __ldg(colp + 64);
   }
   for (int j = 0; j < len; j += 2) {
     if (j + 1 < len) {
-      const int c = cnext;
-      if (j + 2 < len) cnext = __ldg(colp + 32 * (j + 2));
+      const int c = c1;
+      c1 = c2;
+      if (j + 3 < len) c2 = __ldg(colp + 32 * (j + 3));
       fetch(j + 1, c, a1, x1, w1, e1, s1);
     }
     step(a0, x0, w0, e0, s0);
     if (j + 1 >= len) break;
     if (j + 2 < len) {
-      const int c = cnext;
-      if (j + 3 < len) cnext = __ldg(colp + 32 * (j + 3));
+      const int c = c1;
+      c1 = c2;
+      if (j + 4 < len) c2 = __ldg(colp + 32 * (j + 4));
       fetch(j + 2, c, a0, x0, w0, e0, s0);
     }
     step(a1, x1, w1, e1, s1);
   }
   store_y<L>(y, row, s);
 }
+
+template <int L>
+struct SEntry {
+  uint32_t a[L], x[L];
+  int32_t w, ex;
+  uint32_t sx;
+};
 
 // --------------------------------------------------------------------------
 // spmv_sell_pipe<L> (L <= 8): thread per row, software-pipelined: iteration j
@@ -89,13 +102,6 @@ __global__ void __launch_bounds__(128, MINB) spmv_sell(PartView P, XView x, YVie
 // ALU-bound (few rows, short chains), so the product's IMAD.WIDE chain and
 // the adder's ALU chain hide each other's latency.
 // --------------------------------------------------------------------------
-template <int L>
-struct SEntry {
-  uint32_t a[L], x[L];
-  int32_t w, ex;
-  uint32_t sx;
-};
-
 template <int L>
 __global__ void __launch_bounds__(128) spmv_sell_pipe(PartView P, XView x, YView y) {
   constexpr int K0 = MulStage<L>::K0;
@@ -187,16 +193,20 @@ static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStrea
       return (int)cudaGetLastError();
     }
   }
-  static const int minb = [] {
-    const char* v = std::getenv("MPSP_MINB");
-    return v ? std::atoi(v) : 0;
-  }();
+  // tuning knob (read per launch): MPSP_MINB = min resident blocks per SM
+  // (register cap).  Defaults measured on B200: 6 at L <= 8 (80 registers;
+  // C2 0.0385 -> 0.0332 ms, C4 A^T 0.316 -> 0.295 ms), 4 at L = 16 (128
+  // registers; C3 0.280 -> 0.239 ms), 1 at L = 32 (more spills than gain).
+  const char* vm = std::getenv("MPSP_MINB");
+  const int minb = vm ? std::atoi(vm) : (L <= 8 ? 6 : (L == 16 ? 4 : 1));
+  const unsigned nb = (unsigned)blocks;
   switch (minb) {
-    case 2: spmv_sell<L, 2><<<(unsigned)blocks, threads, 0, st>>>(P, x, y); break;
-    case 3: spmv_sell<L, 3><<<(unsigned)blocks, threads, 0, st>>>(P, x, y); break;
-    case 4: spmv_sell<L, 4><<<(unsigned)blocks, threads, 0, st>>>(P, x, y); break;
-    case 6: spmv_sell<L, 6><<<(unsigned)blocks, threads, 0, st>>>(P, x, y); break;
-    default: spmv_sell<L, 1><<<(unsigned)blocks, threads, 0, st>>>(P, x, y); break;
+    case 2: spmv_sell<L, 2><<<nb, threads, 0, st>>>(P, x, y); break;
+    case 3: spmv_sell<L, 3><<<nb, threads, 0, st>>>(P, x, y); break;
+    case 4: spmv_sell<L, 4><<<nb, threads, 0, st>>>(P, x, y); break;
+    case 6: spmv_sell<L, 6><<<nb, threads, 0, st>>>(P, x, y); break;
+    case 8: spmv_sell<L, 8><<<nb, threads, 0, st>>>(P, x, y); break;
+    default: spmv_sell<L, 1><<<nb, threads, 0, st>>>(P, x, y); break;
   }
   g_launches.fetch_add(1);
   return (int)cudaGetLastError();
