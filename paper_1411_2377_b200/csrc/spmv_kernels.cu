@@ -87,6 +87,107 @@ __global__ void __launch_bounds__(128, MINB) spmv_sell(PartView P, XView x, YVie
   store_y<L>(y, row, s);
 }
 
+// --------------------------------------------------------------------------
+// spmv_sell_cp<L> (L = 32): the thread-per-row SELL kernel with the operand
+// prefetch moved out of registers: entry j+1's A limbs and x limbs are copied
+// global -> shared by cp.async (LDGSTS, double-buffered per thread) while
+// entry j is processed, and the accumulator s is parked in shared memory
+// during the product.  At L = 32 the register-prefetching kernel needs ~240
+// registers (8 warps/SM, latency-bound at ~55% of the IMAD.WIDE pipe); this
+// one fits 3 blocks of 128 threads per SM.
+// --------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr int CP_THREADS = 128;
+
+template <int L>
+__global__ void __launch_bounds__(CP_THREADS, 3) spmv_sell_cp(PartView P, XView x, YView y) {
+  constexpr int NC = L / 4;                      // 16-byte chunks per operand
+  extern __shared__ uint4 smc[];                 // [stage][a|x][NC][thread]
+  const int tid = threadIdx.x;
+  const int64_t slot = (int64_t)blockIdx.x * blockDim.x + tid;
+  const bool live = slot < P.nslots;
+  const int row = live ? P.slot_row[slot] : -1;
+  if (row < 0) return;
+  const int len = P.slot_len[slot];
+  const int l = (int)(slot & 31);
+  const int64_t g0 = P.slice_ptr[slot >> 5] >> 5;
+  const int32_t* colp = P.col + g0 * 32 + l;
+  const int32_t* expp = P.expw + g0 * 32 + l;
+  const uint4* A4 = reinterpret_cast<const uint4*>(P.limbs);
+  const uint4* X4 = reinterpret_cast<const uint4*>(x.limbs);
+  auto sa = [&](int st, int c) { return smc + ((st * 2 + 0) * NC + c) * CP_THREADS + tid; };
+  auto sx = [&](int st, int c) { return smc + ((st * 2 + 1) * NC + c) * CP_THREADS + tid; };
+  int32_t wq[2], exq[2];
+  uint32_t sq[2];
+  auto issue = [&](int j, int col, int st) {
+    const uint4* ga = A4 + (g0 + j) * NC * 32 + l;
+    const uint4* gx = X4 + (int64_t)col * NC;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      cp_async16(sa(st, c), ga + c * 32);
+      cp_async16(sx(st, c), gx + c);
+    }
+    cp_async_commit();
+    wq[st] = __ldg(expp + 32 * j);
+    exq[st] = __ldg(x.exps + col);
+    sq[st] = __ldg(x.signs + col);
+  };
+  MP<L> s;
+  s.set_zero();
+  int c1 = 0, c2 = 0;
+  if (len > 0) {
+    issue(0, __ldg(colp), 0);
+    if (len > 1) c1 = __ldg(colp + 32);
+    if (len > 2) c2 = __ldg(colp + 64);
+  }
+  for (int j = 0; j < len; j += 2) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int jj = j + u;
+      if (jj >= len) break;
+      if (jj + 1 < len) {
+        const int c = c1;
+        c1 = c2;
+        if (jj + 3 < len) c2 = __ldg(colp + 32 * (jj + 3));
+        issue(jj + 1, c, u ^ 1);
+        cp_async_wait<1>();                      // entry jj has landed
+      } else {
+        cp_async_wait<0>();
+      }
+      uint32_t a[L], xv[L];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const uint4 va = *sa(u, c), vx = *sx(u, c);
+        a[4 * c] = va.x; a[4 * c + 1] = va.y; a[4 * c + 2] = va.z; a[4 * c + 3] = va.w;
+        xv[4 * c] = vx.x; xv[4 * c + 1] = vx.y; xv[4 * c + 2] = vx.z; xv[4 * c + 3] = vx.w;
+      }
+      // park the accumulator's limbs during the product in this entry's
+      // (already consumed) A slot; the next copy into it is issued only in
+      // the next iteration
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        *sa(u, c) = make_uint4(s.m[4 * c], s.m[4 * c + 1], s.m[4 * c + 2], s.m[4 * c + 3]);
+      MP<L> t;
+      const int32_t ea = (int32_t)((uint32_t)wq[u] << 1) >> 1;
+      mp_mul<L>(a, ea, (uint32_t)wq[u] >> 31, xv, exq[u], sq[u], t);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const uint4 v = *sa(u, c);
+        s.m[4 * c] = v.x; s.m[4 * c + 1] = v.y; s.m[4 * c + 2] = v.z; s.m[4 * c + 3] = v.w;
+      }
+      mp_add<L>(s, t);
+    }
+  }
+  store_y<L>(y, row, s);
+}
+
 template <int L>
 struct SEntry {
   uint32_t a[L], x[L];
@@ -189,6 +290,23 @@ static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStrea
     const bool pipe = v && v[0] == '1';
     if (pipe) {
       spmv_sell_pipe<L><<<(unsigned)blocks, threads, 0, st>>>(P, x, y);
+      g_launches.fetch_add(1);
+      return (int)cudaGetLastError();
+    }
+  }
+  if constexpr (L == 32) {
+    const char* vc = std::getenv("MPSP_CP");       // 0: register-prefetch kernel
+    if (!(vc && vc[0] == '0')) {
+      constexpr int NC = L / 4;
+      const size_t smem = (size_t)4 * NC * CP_THREADS * 16;   // 2 stages x (a, x): 64 KB
+      static bool attr = false;
+      if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(spmv_sell_cp<L>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        attr = true;
+      }
+      spmv_sell_cp<L><<<(unsigned)blocks, CP_THREADS, smem, st>>>(P, x, y);
       g_launches.fetch_add(1);
       return (int)cudaGetLastError();
     }

@@ -249,8 +249,11 @@ struct WChain {
   }
 };
 
+#ifndef MPSP_WROW_MINB
+#define MPSP_WROW_MINB 1
+#endif
 template <int L>
-__global__ void __launch_bounds__(128) spmv_wrow(PartView P, XView x, YView y) {
+__global__ void __launch_bounds__(128, (L <= 8 ? MPSP_WROW_MINB : 1)) spmv_wrow(PartView P, XView x, YView y) {
   const int64_t w = P.npcrow + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (w >= P.nwrow) return;
