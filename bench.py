@@ -349,8 +349,9 @@ def main():
             roof["traffic_source"] = f"profiles/{rec['summary'] or rec['report']} ({rec['kernel']})"
             roof["algorithmic_bytes"] = bytes_local
     thr = int(os.environ.get("MPSP_LONG_T", "128"))
-    roof["kernel"] = (f"spmv_sell<{L}>" if d["meta"]["max_row"] <= thr or args.op == "atx" else
-                      f"spmv_sell<{L}> + spmv_wrow<{L}> (concurrent streams, fork/join timed as one)")
+    sell = f"spmv_sell_cp<{L}>" if L == 32 and os.environ.get("MPSP_CP", "1") != "0" else f"spmv_sell<{L}>"
+    roof["kernel"] = (sell if d["meta"]["max_row"] <= thr or args.op == "atx" else
+                      f"{sell} + spmv_wrow<{L}> (concurrent streams, fork/join timed as one)")
     roof["kernel_ms"] = kern_avg_s * 1e3
     roof["t_roof_ms"] = max(t_mem, t_int) * 1e3
     roof["frac_of_t_roof"] = max(t_mem, t_int) / kern_avg_s

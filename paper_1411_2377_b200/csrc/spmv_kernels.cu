@@ -105,9 +105,13 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 constexpr int CP_THREADS = 128;
+// (L = 16 measured no faster than the register-prefetch kernel with a
+// 128-register cap, so only L = 32 uses this kernel)
+template <int L>
+struct CpMinB { static constexpr int v = L >= 32 ? 3 : 5; };
 
 template <int L>
-__global__ void __launch_bounds__(CP_THREADS, 3) spmv_sell_cp(PartView P, XView x, YView y) {
+__global__ void __launch_bounds__(CP_THREADS, CpMinB<L>::v) spmv_sell_cp(PartView P, XView x, YView y) {
   constexpr int NC = L / 4;                      // 16-byte chunks per operand
   extern __shared__ uint4 smc[];                 // [stage][a|x][NC][thread]
   const int tid = threadIdx.x;
@@ -298,7 +302,7 @@ static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStrea
     const char* vc = std::getenv("MPSP_CP");       // 0: register-prefetch kernel
     if (!(vc && vc[0] == '0')) {
       constexpr int NC = L / 4;
-      const size_t smem = (size_t)4 * NC * CP_THREADS * 16;   // 2 stages x (a, x): 64 KB
+      const size_t smem = (size_t)4 * NC * CP_THREADS * 16;   // 2 stages x (a, x): 16L KB
       static bool attr = false;
       if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(spmv_sell_cp<L>,
