@@ -415,135 +415,4 @@ __device__ __forceinline__ void mp_add(MP<L>& s, const MP<L>& t) {
   s.s = sb;
 }
 
-// --------------------------------------------------------------------------
-// Staged forms of mp_mul / mp_add for software pipelining (spmv_sell_pipe):
-// the product of entry j+1 and the add of entry j are written as phases with
-// no branch inside a phase except the shifter's warp-uniform limb steps, so
-// the scheduler can interleave the product's IMAD.WIDE chain with the add's
-// ALU work.  The rare cases (product certificate fails, >= 32-bit
-// cancellation) only raise a flag; the caller redoes that step with the
-// general mp_mul_full / mp_add.  Results are identical to mp_mul / mp_add.
-// --------------------------------------------------------------------------
-template <int L>
-struct MulStage {
-  static constexpr int K0 = L - 3;
-  uint32_t T[L + 3];
-  uint32_t c0, c1, c2;
-};
-
-// columns [KB, KE) of the short product (KB >= K0)
-template <int L, int KB, int KE>
-__device__ __forceinline__ void mul_cols(const uint32_t (&a)[L], const uint32_t (&x)[L],
-                                         MulStage<L>& M) {
-  constexpr int K0 = MulStage<L>::K0;
-  constexpr int NCH = MulChains<L>::n;
-  if constexpr (KB == K0) { M.c0 = 0u; M.c1 = 0u; M.c2 = 0u; }
-#pragma unroll
-  for (int k = KB; k < KE; ++k) {
-    const int ilo = k - (L - 1) > 0 ? k - (L - 1) : 0;
-    const int ihi = k < L - 1 ? k : L - 1;
-    const int nt = ihi - ilo + 1;
-    uint32_t A0[NCH], A1[NCH], A2[NCH];
-    A0[0] = M.c0; A1[0] = M.c1; A2[0] = M.c2;
-#pragma unroll
-    for (int ch = 1; ch < NCH; ++ch) { A0[ch] = 0u; A1[ch] = 0u; A2[ch] = 0u; }
-#pragma unroll
-    for (int i = 0; i < L; ++i) {
-      if (i < ilo || i > ihi) continue;
-      const int ch = (i - ilo) % NCH;
-      mac3(A0[ch], A1[ch], A2[ch], a[i], x[k - i]);
-    }
-#pragma unroll
-    for (int ch = 1; ch < NCH; ++ch)
-      if (ch < nt) add3w(A0[0], A1[0], A2[0], A0[ch], A1[ch], A2[ch]);
-    M.T[k - K0] = A0[0];
-    M.c0 = A1[0]; M.c1 = A2[0]; M.c2 = 0u;
-  }
-  if constexpr (KE == 2 * L - 1) M.T[2 * L - 1 - K0] = M.c0;
-}
-
-// normalise + round the certified short product; returns true when the
-// certificate fails (caller: mp_mul_full)
-template <int L>
-__device__ __forceinline__ bool mul_finish(const MulStage<L>& M, bool zero, int32_t ea, uint32_t sa,
-                                           int32_t ex, uint32_t sx, MP<L>& t) {
-  const uint32_t sh = (~M.T[L + 2]) >> 31;
-  const uint32_t wmask = (1u << (31u - sh)) - 1u;
-  const uint32_t w1 = M.T[1] >> 5, w2 = M.T[2] & wmask;
-  const bool amb = ((w1 | w2) == 0u) || (w1 == 0x07FFFFFFu && w2 == wmask);
-#pragma unroll
-  for (int i = L - 1; i >= 0; --i) t.m[i] = __funnelshift_l(M.T[i + 2], M.T[i + 3], sh);
-  const uint32_t rb = (M.T[2] << sh) >> 31;
-  const uint32_t cy = inc_n<L>(t.m, rb);
-  t.m[L - 1] = cy ? 0x80000000u : t.m[L - 1];
-  t.e = ea + ex - (int32_t)sh + (int32_t)cy;
-  t.s = sa ^ sx;
-#pragma unroll
-  for (int i = 0; i < L; ++i) t.m[i] = zero ? 0u : t.m[i];
-  return amb && !zero;
-}
-
-template <int L>
-struct AddStage {
-  uint32_t Z[L + 1], Y[L + 1];
-  int32_t eb;
-  uint32_t sb, sub, d, stk;
-};
-
-template <int L>
-__device__ __forceinline__ void add_pre(const MP<L>& s, const MP<L>& t, AddStage<L>& A) {
-  const bool tz = t.is_zero(), sz = s.is_zero();
-  const uint32_t mlt = lt_n<L>(s.m, t.m);
-  const bool t_big = !tz && (sz || t.e > s.e || (t.e == s.e && mlt));
-  A.eb = t_big ? t.e : s.e;
-  const int32_t esm = t_big ? s.e : t.e;
-  A.sb = t_big ? t.s : s.s;
-  A.sub = (t.s != s.s && !tz && !sz) ? 1u : 0u;
-  uint32_t d = (uint32_t)A.eb - (uint32_t)esm;
-  A.d = (tz || sz) ? 0u : min(d, (uint32_t)(32 * (L + 1)));
-  A.Z[0] = 0u;
-  A.Y[0] = 0u;
-#pragma unroll
-  for (int i = 0; i < L; ++i) {
-    A.Z[i + 1] = t_big ? t.m[i] : s.m[i];
-    A.Y[i + 1] = t_big ? s.m[i] : t.m[i];
-  }
-}
-
-template <int L>
-__device__ __forceinline__ void add_align(AddStage<L>& A) {
-  A.stk = 0u;
-  shr_bits_sticky<L + 1>(A.Y, A.d, A.stk);
-}
-
-// returns true for >= 32 bits of cancellation / exact zero (caller: mp_add)
-template <int L>
-__device__ __forceinline__ bool add_post(AddStage<L>& A, MP<L>& out) {
-  const uint32_t msk = 0u - A.sub;
-#pragma unroll
-  for (int i = 0; i <= L; ++i) A.Y[i] ^= msk;
-  const uint32_t cin = A.sub & (A.stk == 0u ? 1u : 0u);
-  const uint32_t W = add_n_cin<L + 1>(A.Z, A.Z, A.Y, cin) & (A.sub ^ 1u);
-  uint32_t stk = A.stk | (A.Z[0] & W);
-#pragma unroll
-  for (int i = 0; i < L; ++i) A.Z[i] = __funnelshift_r(A.Z[i], A.Z[i + 1], W);
-  A.Z[L] = __funnelshift_r(A.Z[L], W, W);
-  const uint32_t lz0 = __clz(A.Z[L]);
-  const bool rare = lz0 >= 32u;
-  const uint32_t lz = rare ? 0u : lz0;
-#pragma unroll
-  for (int i = L; i > 0; --i) A.Z[i] = __funnelshift_l(A.Z[i - 1], A.Z[i], lz);
-  A.Z[0] <<= lz;
-  const int32_t e = A.eb + (int32_t)W - (int32_t)lz;
-  const uint32_t rb = A.Z[0] >> 31;
-  const uint32_t st = stk | (A.Z[0] << 1);
-#pragma unroll
-  for (int i = 0; i < L; ++i) out.m[i] = A.Z[i + 1];
-  const uint32_t cy = rne_increment<L>(out.m, rb, st);
-  out.m[L - 1] = cy ? 0x80000000u : out.m[L - 1];
-  out.e = e + (int32_t)cy;
-  out.s = A.sb;
-  return rare;
-}
-
 }  // namespace mpsp

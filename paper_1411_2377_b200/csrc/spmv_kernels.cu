@@ -107,8 +107,11 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 constexpr int CP_THREADS = 128;
 // (L = 16 measured no faster than the register-prefetch kernel with a
 // 128-register cap, so only L = 32 uses this kernel)
+#ifndef MPSP_CP8_MINB
+#define MPSP_CP8_MINB 8
+#endif
 template <int L>
-struct CpMinB { static constexpr int v = L >= 32 ? 3 : 5; };
+struct CpMinB { static constexpr int v = L >= 32 ? 3 : (L >= 16 ? 5 : MPSP_CP8_MINB); };
 
 template <int L>
 __global__ void __launch_bounds__(CP_THREADS, CpMinB<L>::v) spmv_sell_cp(PartView P, XView x, YView y) {
@@ -193,114 +196,14 @@ __global__ void __launch_bounds__(CP_THREADS, CpMinB<L>::v) spmv_sell_cp(PartVie
 }
 
 template <int L>
-struct SEntry {
-  uint32_t a[L], x[L];
-  int32_t w, ex;
-  uint32_t sx;
-};
-
-// --------------------------------------------------------------------------
-// spmv_sell_pipe<L> (L <= 8): thread per row, software-pipelined: iteration j
-// forms the product of entry j+1 and the rounded add of entry j as
-// interleaved phases of one instruction stream (mp_device.cuh "staged
-// forms"), while entry j+2 is loading.  At L <= 8 the kernel is latency- and
-// ALU-bound (few rows, short chains), so the product's IMAD.WIDE chain and
-// the adder's ALU chain hide each other's latency.
-// --------------------------------------------------------------------------
-template <int L>
-__global__ void __launch_bounds__(128) spmv_sell_pipe(PartView P, XView x, YView y) {
-  constexpr int K0 = MulStage<L>::K0;
-  constexpr int KM = (K0 + 2 * L - 1) / 2;        // product columns split point
-  const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (slot >= P.nslots) return;
-  const int row = P.slot_row[slot];
-  if (row < 0) return;
-  const int len = P.slot_len[slot];
-  const int l = (int)(slot & 31);
-  const int64_t g0 = P.slice_ptr[slot >> 5] >> 5;
-  const int32_t* colp = P.col + g0 * 32 + l;
-  const int32_t* expp = P.expw + g0 * 32 + l;
-  auto fetch = [&](int j, int col, SEntry<L>& E) {
-    E.w = __ldg(expp + 32 * j);
-    load_a<L>(P.limbs, g0 + j, l, E.a);
-    load_x<L>(x.limbs, col, E.x);
-    E.ex = __ldg(x.exps + col);
-    E.sx = __ldg(x.signs + col);
-  };
-  auto full_mul = [&](const SEntry<L>& E, MP<L>& t) {
-    const int32_t ea = (int32_t)((uint32_t)E.w << 1) >> 1;
-    mp_mul<L>(E.a, ea, (uint32_t)E.w >> 31, E.x, E.ex, E.sx, t);
-  };
-  MP<L> s;
-  s.set_zero();
-  if (len > 0) {
-    MP<L> tc;                                     // product of entry j
-    SEntry<L> B0, B1;                             // entries j+1, j+2
-    int cn = 0;                                   // column of the entry after
-    {
-      SEntry<L> E0;
-      fetch(0, __ldg(colp), E0);
-      if (len > 1) fetch(1, __ldg(colp + 32), B0);
-      if (len > 2) cn = __ldg(colp + 64);
-      full_mul(E0, tc);
-    }
-    // one pipelined iteration: add tc, product of Bc (entry j+1) -> tc,
-    // loads of entry j+2 into Bn
-    auto iter = [&](int j, SEntry<L>& Bc, SEntry<L>& Bn) {
-      const bool more = j + 1 < len;
-      if (j + 2 < len) {
-        const int c = cn;
-        if (j + 3 < len) cn = __ldg(colp + 32 * (j + 3));
-        fetch(j + 2, c, Bn);
-      }
-      MulStage<L> M;
-      AddStage<L> A;
-      MP<L> sn, tn;
-      // phase 1: compare/swap of the add, first product columns
-      add_pre<L>(s, tc, A);
-      if (more) mul_cols<L, K0, KM>(Bc.a, Bc.x, M);
-      add_align<L>(A);
-      // phase 2: the rest of both
-      if (more) mul_cols<L, KM, 2 * L - 1>(Bc.a, Bc.x, M);
-      const bool ra = add_post<L>(A, sn);
-      const int32_t ea = (int32_t)((uint32_t)Bc.w << 1) >> 1;
-      const bool zero = (Bc.a[L - 1] == 0u) || (Bc.x[L - 1] == 0u);
-      const bool rm = more && mul_finish<L>(M, zero, ea, (uint32_t)Bc.w >> 31, Bc.ex, Bc.sx, tn);
-      if (ra | rm) {                              // rare: exact general paths
-        if (ra) { sn = s; mp_add<L>(sn, tc); }
-        if (rm) full_mul(Bc, tn);
-      }
-      s = sn;
-      tc = tn;
-    };
-    for (int j = 0; j < len; j += 2) {
-      iter(j, B0, B1);
-      if (j + 1 >= len) break;
-      iter(j + 1, B1, B0);
-    }
-  }
-  store_y<L>(y, row, s);
-}
-
-template <int L>
 static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStream_t st) {
   const int64_t nshort = P.nslots;
   if (nshort <= 0) return 0;
   const int threads = 128;
   const int64_t blocks = (nshort + threads - 1) / threads;
-  if constexpr (L >= 4 && L <= 8) {
-    // opt-in (MPSP_PIPE=1): measured slower than spmv_sell on short rows
-    const char* v = std::getenv("MPSP_PIPE");    // read per launch (tests toggle it)
-    const bool pipe = v && v[0] == '1';
-    if (pipe) {
-      spmv_sell_pipe<L><<<(unsigned)blocks, threads, 0, st>>>(P, x, y);
-      g_launches.fetch_add(1);
-      return (int)cudaGetLastError();
-    }
-  }
-  if constexpr (L == 32) {
+  if constexpr (L == 32 || L == 8) {
     const char* vc = std::getenv("MPSP_CP");       // 0: register-prefetch kernel
-    if (!(vc && vc[0] == '0')) {
+    if (L == 32 ? !(vc && vc[0] == '0') : (vc && vc[0] == '1')) {
       constexpr int NC = L / 4;
       const size_t smem = (size_t)4 * NC * CP_THREADS * 16;   // 2 stages x (a, x): 16L KB
       static bool attr = false;
@@ -326,6 +229,7 @@ static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStrea
     case 2: spmv_sell<L, 2><<<nb, threads, 0, st>>>(P, x, y); break;
     case 3: spmv_sell<L, 3><<<nb, threads, 0, st>>>(P, x, y); break;
     case 4: spmv_sell<L, 4><<<nb, threads, 0, st>>>(P, x, y); break;
+    case 5: spmv_sell<L, 5><<<nb, threads, 0, st>>>(P, x, y); break;
     case 6: spmv_sell<L, 6><<<nb, threads, 0, st>>>(P, x, y); break;
     case 8: spmv_sell<L, 8><<<nb, threads, 0, st>>>(P, x, y); break;
     default: spmv_sell<L, 1><<<nb, threads, 0, st>>>(P, x, y); break;

@@ -296,15 +296,140 @@ __global__ void __launch_bounds__(128, (L <= 8 ? MPSP_WROW_MINB : 1)) spmv_wrow(
 }
 
 // --------------------------------------------------------------------------
-// spmv_pcrow<L>: the longest rows, one CTA per row.  Warp 0 runs the chain
-// (WChain::consume, 32 steps per block); warps 1..PCP compute the products
-// (block b by producer b % PCP) into a double-buffered shared-memory slot
-// per producer, handed over with named barriers (FULL: producer -> chain,
-// EMPTY: chain -> producer).  The chain warp then only pays the block sum,
-// so a 5000-long row's critical path is ~157 block sums.
+// spmv_pcrow<L>: the longest rows, one CTA per row, products and chain in
+// different warps.  U = pc_spl(L) producer warps: producer u computes, for
+// every 32U-step chunk, the products of steps Uk + u (k = lane; consecutive
+// entries in the chunk-permuted layout, layout.h) into a double-buffered
+// shared-memory slot; FULL / EMPTY named barriers hand the slots over.  The
+// chain warp runs WChainU::consume: lane k owns the U consecutive steps
+// Uk .. Uk+U-1, so one block sum (one warp scan, one ballot) advances the
+// chain 32U steps and the U per-lane alignments are independent (ILP).
+// A tie on the grid is handled as a failing step (exact path).
 // --------------------------------------------------------------------------
-constexpr int PCP = 3;                               // producer warps
-constexpr int PC_THREADS = 32 * (PCP + 1);
+template <int L, int U>
+__device__ __forceinline__ void select_mp(const MP<L> (&t)[U], int u, MP<L>& o) {
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    uint32_t v = t[0].m[i];
+#pragma unroll
+    for (int k = 1; k < U; ++k) v = (u == k) ? t[k].m[i] : v;
+    o.m[i] = v;
+  }
+  int32_t e = t[0].e;
+  uint32_t sg = t[0].s;
+#pragma unroll
+  for (int k = 1; k < U; ++k) {
+    e = (u == k) ? t[k].e : e;
+    sg = (u == k) ? t[k].s : sg;
+  }
+  o.e = e;
+  o.s = sg;
+}
+
+template <int L, int U>
+__device__ __forceinline__ void consume_u(WChain<L>& ch, const MP<L> (&t)[U], int lane) {
+  constexpr int N = L + 2;
+  constexpr int CS = 32 * U;
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int32_t LO = 1 << (HB - 1), HI = 1 << HB;
+  bool tz[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) tz[u] = t[u].is_zero();
+  int start = 0;
+  while (start < CS) {
+    if (ch.szero) {
+      int fu = U;
+#pragma unroll
+      for (int u = U - 1; u >= 0; --u)
+        if (!tz[u] && U * lane + u >= start) fu = u;
+      const unsigned nzm = __ballot_sync(FULL, fu < U);
+      if (nzm == 0u) break;
+      const int kf = __ffs(nzm) - 1;
+      const int uf = __shfl_sync(FULL, fu, kf);
+      MP<L> tsel, tf;
+      select_mp<L, U>(t, uf, tsel);
+#pragma unroll
+      for (int i = 0; i < L; ++i) tf.m[i] = __shfl_sync(FULL, tsel.m[i], kf);
+      tf.e = __shfl_sync(FULL, tsel.e, kf);
+      tf.s = __shfl_sync(FULL, tsel.s, kf);
+      ch.reset_to(tf, lane);
+      start = U * kf + uf + 1;
+      continue;
+    }
+    uint32_t Q[U][N];
+    int32_t h[U];
+    bool act[U], pre[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      act[u] = (U * lane + u >= start) && !tz[u];
+      const int64_t d64 = (int64_t)ch.E - (int64_t)t[u].e;
+      const bool badd = act[u] && d64 < 1;
+      const bool use = act[u] && !badd;
+      const uint32_t dd = use ? (uint32_t)min(d64, (int64_t)(32 * L + 32)) : 0u;
+      uint32_t Y[L + 1];
+      Y[0] = 0u;
+#pragma unroll
+      for (int i = 0; i < L; ++i) Y[i + 1] = t[u].m[i];
+      uint32_t stk = 0u;
+      shr_bits_sticky<L + 1>(Y, dd, stk);
+      const uint32_t rb = Y[0] >> 31;
+      const bool sticky = (stk | (Y[0] << 1)) != 0u;
+      const bool tie = use && rb && !sticky;
+      const uint32_t inc = (rb && sticky) ? 1u : 0u;
+      pre[u] = badd || tie;
+      const uint32_t neg = (use && t[u].s != ch.sg) ? 1u : 0u;
+      const uint32_t nm = 0u - neg;
+#pragma unroll
+      for (int i = 0; i < L; ++i) Q[u][i] = (use ? Y[i + 1] : 0u) ^ nm;
+      Q[u][L] = nm;
+      Q[u][L + 1] = nm;
+      inc_n<N>(Q[u], use ? (neg ? 1u - inc : inc) : 0u);
+      h[u] = hi_of_q<L>(Q[u]);
+    }
+    int32_t Hx[U];
+    int32_t tot = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) { Hx[u] = tot; tot += h[u]; }
+    int32_t Pi = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t v = __shfl_up_sync(FULL, Pi, o);
+      if (lane >= o) Pi += v;
+    }
+    const int32_t X = ch.Shi + Pi - tot;
+    int fu = U;
+#pragma unroll
+    for (int u = U - 1; u >= 0; --u) {
+      const int32_t LB = X + Hx[u];
+      const int32_t ek = ch.err + U * lane + u;
+      const bool ok = !act[u] || (!pre[u] && LB + h[u] - 1 >= LO && LB + ek + h[u] + 1 <= HI);
+      if (!ok) fu = u;
+    }
+    const unsigned failM = __ballot_sync(FULL, fu < U);
+    if (failM == 0u) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) add_n<N>(ch.R, ch.R, Q[u]);
+      ch.Shi += __shfl_sync(FULL, Pi, 31);
+      ch.err = min(ch.err + CS, 1 << 28);
+      break;
+    }
+    const int kf = __ffs(failM) - 1;
+    const int uf = __shfl_sync(FULL, fu, kf);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (lane < kf || (lane == kf && u < uf)) add_n<N>(ch.R, ch.R, Q[u]);
+    MP<L> s, tsel, tf;
+    ch.exact(s);
+    select_mp<L, U>(t, uf, tsel);
+#pragma unroll
+    for (int i = 0; i < L; ++i) tf.m[i] = __shfl_sync(FULL, tsel.m[i], kf);
+    tf.e = __shfl_sync(FULL, tsel.e, kf);
+    tf.s = __shfl_sync(FULL, tsel.s, kf);
+    mp_add<L>(s, tf);
+    ch.reset_to(s, lane);
+    start = U * kf + uf + 1;
+  }
+}
 
 __device__ __forceinline__ void bar_sync_n(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -314,53 +439,78 @@ __device__ __forceinline__ void bar_arrive_n(int id, int n) {
 }
 
 template <int L>
-__global__ void __launch_bounds__(PC_THREADS) spmv_pcrow(PartView P, XView x, YView y) {
+__global__ void __launch_bounds__(32 * (1 + pc_spl(L))) spmv_pcrow(PartView P, XView x, YView y) {
+  constexpr int U = pc_spl(L);
+  constexpr int CS = 32 * U;
   constexpr int SW = L + 2;                          // words per product
-  __shared__ uint32_t slot[PCP][2][SW][32];          // [producer][buffer][word][lane]
+  constexpr int NT = 32 * (U + 1);                   // barrier participants
+  __shared__ uint32_t slot[2][SW][U][32];            // [buffer][word][u][lane]
   const int64_t w = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t e0 = P.wrow_ptr[w];
   const int len = P.wrow_len[w];
-  const int nblk = (len + 31) / 32;
+  const int nch = (len + CS - 1) / CS;
   if (warp > 0) {
-    const int p = warp - 1;
+    // producer u: positions c*CS + 32u + lane, step c*CS + U*lane + u
+    const int u = warp - 1;
+    auto colof = [&](int c) {
+      return (c * CS + U * lane + u < len) ? __ldg(P.col + e0 + c * CS + 32 * u + lane) : 0;
+    };
+    auto load = [&](int c, int col, WEntry<L>& E) {
+      E.valid = c * CS + U * lane + u < len;
+      if (!E.valid) {
+#pragma unroll
+        for (int i = 0; i < L; ++i) { E.a[i] = 0u; E.x[i] = 0u; }
+        E.w = 0; E.ex = 0; E.sx = 0u;
+        return;
+      }
+      const int64_t e = e0 + c * CS + 32 * u + lane;
+      E.w = __ldg(P.expw + e);
+      load_a<L>(P.limbs, e >> 5, lane, E.a);
+      load_x<L>(x.limbs, col, E.x);
+      E.ex = __ldg(x.exps + col);
+      E.sx = __ldg(x.signs + col);
+    };
     WEntry<L> nxt;
     int cnext = 0;
-    if (p < nblk) {
-      wload<L>(P, x, e0, 32 * p, len, lane, wcol(P, e0, 32 * p, len, lane), nxt);
-      cnext = wcol(P, e0, 32 * (p + PCP), len, lane);
+    if (nch > 0) {
+      load(0, colof(0), nxt);
+      cnext = colof(1);
     }
-    for (int b = p, i = 0; b < nblk; b += PCP, ++i) {
-      const int j = i & 1;
+    for (int c = 0; c < nch; ++c) {
+      const int j = c & 1;
       WEntry<L> cur = nxt;
-      if (b + PCP < nblk) {
-        wload<L>(P, x, e0, 32 * (b + PCP), len, lane, cnext, nxt);
-        cnext = wcol(P, e0, 32 * (b + 2 * PCP), len, lane);
+      if (c + 1 < nch) {
+        load(c + 1, cnext, nxt);
+        cnext = colof(c + 2);
       }
       MP<L> t;
       const int32_t ea = (int32_t)((uint32_t)cur.w << 1) >> 1;
       mp_mul<L>(cur.a, ea, (uint32_t)cur.w >> 31, cur.x, cur.ex, cur.sx, t);
-      if (i >= 2) bar_sync_n(1 + PCP * 2 + 2 * p + j, 64);      // EMPTY(p, j)
+      if (c >= 2) bar_sync_n(3 + j, NT);                       // EMPTY(j)
 #pragma unroll
-      for (int k = 0; k < L; ++k) slot[p][j][k][lane] = t.m[k];
-      slot[p][j][L][lane] = (uint32_t)t.e;
-      slot[p][j][L + 1][lane] = t.s;
-      bar_arrive_n(1 + 2 * p + j, 64);                           // FULL(p, j)
+      for (int k = 0; k < L; ++k) slot[j][k][u][lane] = t.m[k];
+      slot[j][L][u][lane] = (uint32_t)t.e;
+      slot[j][L + 1][u][lane] = t.s;
+      bar_arrive_n(1 + j, NT);                                 // FULL(j)
     }
     return;
   }
   WChain<L> ch;
   ch.init();
-  for (int b = 0; b < nblk; ++b) {
-    const int p = b % PCP, i = b / PCP, j = i & 1;
-    bar_sync_n(1 + 2 * p + j, 64);                               // FULL(p, j)
-    MP<L> t;
+  for (int c = 0; c < nch; ++c) {
+    const int j = c & 1;
+    bar_sync_n(1 + j, NT);                                     // FULL(j)
+    MP<L> t[U];
 #pragma unroll
-    for (int k = 0; k < L; ++k) t.m[k] = slot[p][j][k][lane];
-    t.e = (int32_t)slot[p][j][L][lane];
-    t.s = slot[p][j][L + 1][lane];
-    if (b + 2 * PCP < nblk) bar_arrive_n(1 + PCP * 2 + 2 * p + j, 64);   // EMPTY(p, j)
-    ch.consume(t, lane);
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int k = 0; k < L; ++k) t[u].m[k] = slot[j][k][u][lane];
+      t[u].e = (int32_t)slot[j][L][u][lane];
+      t[u].s = slot[j][L + 1][u][lane];
+    }
+    if (c + 2 < nch) bar_arrive_n(3 + j, NT);                  // EMPTY(j)
+    consume_u<L, U>(ch, t, lane);
   }
   MP<L> s;
   ch.exact(s);
@@ -382,7 +532,7 @@ static int launch_wrow_L(const PartView& P, const XView& x, const YView& y, cuda
 template <int L>
 static int launch_pcrow_L(const PartView& P, const XView& x, const YView& y, cudaStream_t st) {
   if (P.npcrow <= 0) return 0;
-  spmv_pcrow<L><<<(unsigned)P.npcrow, PC_THREADS, 0, st>>>(P, x, y);
+  spmv_pcrow<L><<<(unsigned)P.npcrow, 32 * (1 + pc_spl(L)), 0, st>>>(P, x, y);
   launch_counter_add(1);
   return (int)cudaGetLastError();
 }

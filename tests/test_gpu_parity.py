@@ -185,12 +185,3 @@ def test_pc_threshold_split_c4(pc, monkeypatch):
     d = gen.make("C4", n=20_000, seed=10)
     for op in ("ax", "atx"):
         assert_same(gpu_run(d, op), oracle_full(d, op), f"C4 pc threshold {pc} {op}")
-
-
-@pytest.mark.parametrize("p", [128, 256])
-def test_pipelined_sell_kernel(p, monkeypatch):
-    """MPSP_PIPE=1 selects the software-pipelined SELL kernel at L <= 8."""
-    monkeypatch.setenv("MPSP_PIPE", "1")
-    d = gen.stress(p, seed=12)
-    for op in ("ax", "atx"):
-        assert_same(gpu_run(d, op), oracle_full(d, op), f"pipelined stress p={p} {op}")

@@ -107,9 +107,11 @@ def test_short_product_tie_is_never_certified():
 HB = 26
 
 
-def block_sum_chain(ts, p, G=32):
+def block_sum_chain(ts, p, G=32, ties_exact=False):
     """Model of spmv_wrow's chain over the products ts (oracle triples),
-    G steps per block.  Returns (result, n_fast_steps)."""
+    G steps per block.  ties_exact=True models spmv_pcrow's chain warp, which
+    sends a grid tie through the exact path instead of resolving its parity.
+    Returns (result, n_fast_steps)."""
     L = p // 32
     S, E, sg, zero = 0, 0, 0, True         # exact S (grid integer), exponent, sign
     Shi, err, par = 0, 0, 0
@@ -153,7 +155,7 @@ def block_sum_chain(ts, p, G=32):
                 inc = 1 if rem > half else 0
                 Q.append((Y, inc, st != sg))
                 ties.append(tie)
-                bad.append(False)
+                bad.append(tie and ties_exact)
             # tie parity, then signed Q, then the conservative checks
             p_run = par
             for k in range(len(blk)):
@@ -249,3 +251,5 @@ def test_block_sum_ties_cancellation_and_zeros(p):
                 ts.append(_rand_t(rng, p, s_e - 6, s_e + 2))
         got, _ = block_sum_chain(ts, p, G=rng.choice([4, 32]))
         assert got == oracle_chain(ts, p), trial
+        got, _ = block_sum_chain(ts, p, G=rng.choice([64, 128]), ties_exact=True)
+        assert got == oracle_chain(ts, p), ("ties exact", trial)
