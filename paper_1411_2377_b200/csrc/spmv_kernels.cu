@@ -105,13 +105,10 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 constexpr int CP_THREADS = 128;
-// (L = 16 measured no faster than the register-prefetch kernel with a
-// 128-register cap, so only L = 32 uses this kernel)
-#ifndef MPSP_CP8_MINB
-#define MPSP_CP8_MINB 8
-#endif
+// (L = 16 with 5 blocks/SM and L = 8 with 8 blocks/SM measured no faster than
+// the register-prefetch kernel, so only L = 32 uses this kernel)
 template <int L>
-struct CpMinB { static constexpr int v = L >= 32 ? 3 : (L >= 16 ? 5 : MPSP_CP8_MINB); };
+struct CpMinB { static constexpr int v = 3; };
 
 template <int L>
 __global__ void __launch_bounds__(CP_THREADS, CpMinB<L>::v) spmv_sell_cp(PartView P, XView x, YView y) {
@@ -201,9 +198,9 @@ static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStrea
   if (nshort <= 0) return 0;
   const int threads = 128;
   const int64_t blocks = (nshort + threads - 1) / threads;
-  if constexpr (L == 32 || L == 8) {
+  if constexpr (L == 32) {
     const char* vc = std::getenv("MPSP_CP");       // 0: register-prefetch kernel
-    if (L == 32 ? !(vc && vc[0] == '0') : (vc && vc[0] == '1')) {
+    if (!(vc && vc[0] == '0')) {
       constexpr int NC = L / 4;
       const size_t smem = (size_t)4 * NC * CP_THREADS * 16;   // 2 stages x (a, x): 16L KB
       static bool attr = false;
