@@ -29,7 +29,10 @@ namespace mpsp {
 // consecutive steps Uk .. Uk+U-1 of each 32U-step chunk.  Step j of such a row
 // (chunk c = j/(32U), q = j%(32U)) is stored at position c*32U + 32(q%U) +
 // q/U, so producer warp u's 32 loads of a chunk are consecutive entries.
-__host__ __device__ constexpr int pc_spl(int L) { return L <= 8 ? 4 : (L <= 16 ? 2 : 1); }
+#ifndef MPSP_PC_U
+#define MPSP_PC_U 4
+#endif
+__host__ __device__ constexpr int pc_spl(int L) { return L <= 8 ? MPSP_PC_U : (L <= 16 ? 2 : 1); }
 
 struct PartView {
   const int64_t* slice_ptr;   // [nslices+1] entry offsets (multiples of 32)

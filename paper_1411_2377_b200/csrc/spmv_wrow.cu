@@ -306,35 +306,71 @@ __global__ void __launch_bounds__(128, (L <= 8 ? MPSP_WROW_MINB : 1)) spmv_wrow(
 // chain 32U steps and the U per-lane alignments are independent (ILP).
 // A tie on the grid is handled as a failing step (exact path).
 // --------------------------------------------------------------------------
-template <int L, int U>
-__device__ __forceinline__ void select_mp(const MP<L> (&t)[U], int u, MP<L>& o) {
+// Grid alignment of one product against the accumulator tag (E, sg): Q =
+// +-RN_int(|t|/u) in (L+2)-limb two's complement, its high part, and whether
+// the step must take the exact path (|t| reaches the binade, or a grid tie).
+template <int L>
+__device__ __forceinline__ void align_q(const MP<L>& t, bool act, int32_t E, uint32_t sg,
+                                        uint32_t (&Q)[L + 2], int32_t& h, bool& pre) {
+  constexpr int N = L + 2;
+  const int64_t d64 = (int64_t)E - (int64_t)t.e;
+  const bool badd = act && d64 < 1;
+  const bool use = act && !badd;
+  const uint32_t dd = use ? (uint32_t)min(d64, (int64_t)(32 * L + 32)) : 0u;
+  uint32_t Y[L + 1];
+  Y[0] = 0u;
 #pragma unroll
-  for (int i = 0; i < L; ++i) {
-    uint32_t v = t[0].m[i];
+  for (int i = 0; i < L; ++i) Y[i + 1] = t.m[i];
+  uint32_t stk = 0u;
+  shr_bits_sticky<L + 1>(Y, dd, stk);
+  const uint32_t rb = Y[0] >> 31;
+  const bool sticky = (stk | (Y[0] << 1)) != 0u;
+  const bool tie = use && rb && !sticky;
+  const uint32_t inc = (rb && sticky) ? 1u : 0u;
+  pre = badd || tie;
+  const uint32_t neg = (use && t.s != sg) ? 1u : 0u;
+  const uint32_t nm = 0u - neg;
 #pragma unroll
-    for (int k = 1; k < U; ++k) v = (u == k) ? t[k].m[i] : v;
-    o.m[i] = v;
-  }
-  int32_t e = t[0].e;
-  uint32_t sg = t[0].s;
-#pragma unroll
-  for (int k = 1; k < U; ++k) {
-    e = (u == k) ? t[k].e : e;
-    sg = (u == k) ? t[k].s : sg;
-  }
-  o.e = e;
-  o.s = sg;
+  for (int i = 0; i < L; ++i) Q[i] = (use ? Y[i + 1] : 0u) ^ nm;
+  Q[L] = nm;
+  Q[L + 1] = nm;
+  inc_n<N>(Q, use ? (neg ? 1u - inc : inc) : 0u);
+  h = hi_of_q<L>(Q);
 }
 
+// Shared-memory chunk of the producer/consumer kernel: per step the raw
+// product and its speculative alignment against the tag the producer read.
 template <int L, int U>
-__device__ __forceinline__ void consume_u(WChain<L>& ch, const MP<L> (&t)[U], int lane) {
+struct PcSlot {
+  uint32_t m[L][U][32];         // raw product mantissa (exact path)
+  uint32_t e[U][32], s[U][32];
+  uint32_t q[L + 2][U][32];     // aligned, rounded, signed Q
+  int32_t h[U][32];
+  uint32_t fl[U][32];           // bit0: pre (exact path), bit1: nonzero
+  int32_t tagE[U];              // the tag each producer item aligned to
+  uint32_t tagS[U], tagZ[U];
+};
+
+// The chain over one 32U-step chunk, lane k owning steps Uk .. Uk+U-1.  The
+// first pass uses the producers' pre-aligned Q where their tag equals the
+// chain's state; any restart (after an exact step changed the binade)
+// re-aligns from the raw products.
+template <int L, int U>
+__device__ __forceinline__ void consume_slot(WChain<L>& ch, const PcSlot<L, U>& S, int lane) {
   constexpr int N = L + 2;
   constexpr int CS = 32 * U;
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int32_t LO = 1 << (HB - 1), HI = 1 << HB;
   bool tz[U];
 #pragma unroll
-  for (int u = 0; u < U; ++u) tz[u] = t[u].is_zero();
+  for (int u = 0; u < U; ++u) tz[u] = !(S.fl[u][lane] & 2u);
+  auto prod = [&](int u, MP<L>& t) {
+#pragma unroll
+    for (int i = 0; i < L; ++i) t.m[i] = S.m[i][u][lane];
+    t.e = (int32_t)S.e[u][lane];
+    t.s = S.s[u][lane];
+  };
+  bool first = true;
   int start = 0;
   while (start < CS) {
     if (ch.szero) {
@@ -346,14 +382,14 @@ __device__ __forceinline__ void consume_u(WChain<L>& ch, const MP<L> (&t)[U], in
       if (nzm == 0u) break;
       const int kf = __ffs(nzm) - 1;
       const int uf = __shfl_sync(FULL, fu, kf);
-      MP<L> tsel, tf;
-      select_mp<L, U>(t, uf, tsel);
+      MP<L> tf;
 #pragma unroll
-      for (int i = 0; i < L; ++i) tf.m[i] = __shfl_sync(FULL, tsel.m[i], kf);
-      tf.e = __shfl_sync(FULL, tsel.e, kf);
-      tf.s = __shfl_sync(FULL, tsel.s, kf);
+      for (int i = 0; i < L; ++i) tf.m[i] = S.m[i][uf][kf];
+      tf.e = (int32_t)S.e[uf][kf];
+      tf.s = S.s[uf][kf];
       ch.reset_to(tf, lane);
       start = U * kf + uf + 1;
+      first = false;
       continue;
     }
     uint32_t Q[U][N];
@@ -362,30 +398,19 @@ __device__ __forceinline__ void consume_u(WChain<L>& ch, const MP<L> (&t)[U], in
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       act[u] = (U * lane + u >= start) && !tz[u];
-      const int64_t d64 = (int64_t)ch.E - (int64_t)t[u].e;
-      const bool badd = act[u] && d64 < 1;
-      const bool use = act[u] && !badd;
-      const uint32_t dd = use ? (uint32_t)min(d64, (int64_t)(32 * L + 32)) : 0u;
-      uint32_t Y[L + 1];
-      Y[0] = 0u;
+      const bool tag_ok = first && !S.tagZ[u] && S.tagE[u] == ch.E && S.tagS[u] == ch.sg;
+      if (tag_ok) {                               // warp-uniform
 #pragma unroll
-      for (int i = 0; i < L; ++i) Y[i + 1] = t[u].m[i];
-      uint32_t stk = 0u;
-      shr_bits_sticky<L + 1>(Y, dd, stk);
-      const uint32_t rb = Y[0] >> 31;
-      const bool sticky = (stk | (Y[0] << 1)) != 0u;
-      const bool tie = use && rb && !sticky;
-      const uint32_t inc = (rb && sticky) ? 1u : 0u;
-      pre[u] = badd || tie;
-      const uint32_t neg = (use && t[u].s != ch.sg) ? 1u : 0u;
-      const uint32_t nm = 0u - neg;
-#pragma unroll
-      for (int i = 0; i < L; ++i) Q[u][i] = (use ? Y[i + 1] : 0u) ^ nm;
-      Q[u][L] = nm;
-      Q[u][L + 1] = nm;
-      inc_n<N>(Q[u], use ? (neg ? 1u - inc : inc) : 0u);
-      h[u] = hi_of_q<L>(Q[u]);
+        for (int i = 0; i < N; ++i) Q[u][i] = act[u] ? S.q[i][u][lane] : 0u;
+        h[u] = act[u] ? S.h[u][lane] : 0;
+        pre[u] = (S.fl[u][lane] & 1u) != 0u;
+      } else {
+        MP<L> t;
+        prod(u, t);
+        align_q<L>(t, act[u], ch.E, ch.sg, Q[u], h[u], pre[u]);
+      }
     }
+    first = false;
     int32_t Hx[U];
     int32_t tot = 0;
 #pragma unroll
@@ -418,15 +443,14 @@ __device__ __forceinline__ void consume_u(WChain<L>& ch, const MP<L> (&t)[U], in
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (lane < kf || (lane == kf && u < uf)) add_n<N>(ch.R, ch.R, Q[u]);
-    MP<L> s, tsel, tf;
-    ch.exact(s);
-    select_mp<L, U>(t, uf, tsel);
+    MP<L> sx, tf;
+    ch.exact(sx);
 #pragma unroll
-    for (int i = 0; i < L; ++i) tf.m[i] = __shfl_sync(FULL, tsel.m[i], kf);
-    tf.e = __shfl_sync(FULL, tsel.e, kf);
-    tf.s = __shfl_sync(FULL, tsel.s, kf);
-    mp_add<L>(s, tf);
-    ch.reset_to(s, lane);
+    for (int i = 0; i < L; ++i) tf.m[i] = S.m[i][uf][kf];
+    tf.e = (int32_t)S.e[uf][kf];
+    tf.s = S.s[uf][kf];
+    mp_add<L>(sx, tf);
+    ch.reset_to(sx, lane);
     start = U * kf + uf + 1;
   }
 }
@@ -438,18 +462,33 @@ __device__ __forceinline__ void bar_arrive_n(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// --------------------------------------------------------------------------
+// spmv_pcrow<L>: the longest rows, one CTA per row, products and chain in
+// different warps.  U = pc_spl(L) producer warps: producer u computes, for
+// every 32U-step chunk, the products of steps Uk + u (k = lane; consecutive
+// entries in the chunk-permuted layout, layout.h) AND their grid alignment
+// against the chain's last published tag (E, sign) - a speculation, since the
+// binade changes rarely - into a double-buffered shared-memory slot handed
+// over with FULL / EMPTY named barriers.  The chain warp (WChain, lane k
+// owning steps Uk .. Uk+U-1) checks the tag, scans, bounds and commits a
+// 32U-step block per pass; stale tags and restarts re-align locally from the
+// raw products.  A grid tie takes the exact path.
+// --------------------------------------------------------------------------
 template <int L>
 __global__ void __launch_bounds__(32 * (1 + pc_spl(L))) spmv_pcrow(PartView P, XView x, YView y) {
   constexpr int U = pc_spl(L);
   constexpr int CS = 32 * U;
-  constexpr int SW = L + 2;                          // words per product
   constexpr int NT = 32 * (U + 1);                   // barrier participants
-  __shared__ uint32_t slot[2][SW][U][32];            // [buffer][word][u][lane]
+  extern __shared__ __align__(16) unsigned char pc_smem[];
+  PcSlot<L, U>* slot = reinterpret_cast<PcSlot<L, U>*>(pc_smem);   // [2]
+  volatile int32_t* pub = reinterpret_cast<volatile int32_t*>(slot + 2);   // E, sign, zero
   const int64_t w = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t e0 = P.wrow_ptr[w];
   const int len = P.wrow_len[w];
   const int nch = (len + CS - 1) / CS;
+  if (threadIdx.x == 0) { pub[0] = 0; pub[1] = 0; pub[2] = 1; }
+  __syncthreads();
   if (warp > 0) {
     // producer u: positions c*CS + 32u + lane, step c*CS + U*lane + u
     const int u = warp - 1;
@@ -487,11 +526,29 @@ __global__ void __launch_bounds__(32 * (1 + pc_spl(L))) spmv_pcrow(PartView P, X
       MP<L> t;
       const int32_t ea = (int32_t)((uint32_t)cur.w << 1) >> 1;
       mp_mul<L>(cur.a, ea, (uint32_t)cur.w >> 31, cur.x, cur.ex, cur.sx, t);
+      // speculative alignment against the chain's last published tag
+      const int32_t tE = pub[0];
+      const uint32_t tS = (uint32_t)pub[1], tZ = (uint32_t)pub[2];
+      const int32_t tE0 = __shfl_sync(0xffffffffu, tE, 0);          // one tag per item
+      const uint32_t tS0 = __shfl_sync(0xffffffffu, tS, 0), tZ0 = __shfl_sync(0xffffffffu, tZ, 0);
+      uint32_t Q[L + 2];
+      int32_t h = 0;
+      bool pre = true;
+      const bool nz = !t.is_zero();
+      if (!tZ0) align_q<L>(t, nz, tE0, tS0, Q, h, pre);
       if (c >= 2) bar_sync_n(3 + j, NT);                       // EMPTY(j)
+      PcSlot<L, U>& S = slot[j];
 #pragma unroll
-      for (int k = 0; k < L; ++k) slot[j][k][u][lane] = t.m[k];
-      slot[j][L][u][lane] = (uint32_t)t.e;
-      slot[j][L + 1][u][lane] = t.s;
+      for (int k = 0; k < L; ++k) S.m[k][u][lane] = t.m[k];
+      S.e[u][lane] = (uint32_t)t.e;
+      S.s[u][lane] = t.s;
+      if (!tZ0) {
+#pragma unroll
+        for (int k = 0; k < L + 2; ++k) S.q[k][u][lane] = Q[k];
+        S.h[u][lane] = h;
+      }
+      S.fl[u][lane] = (pre ? 1u : 0u) | (nz ? 2u : 0u);
+      if (lane == 0) { S.tagE[u] = tE0; S.tagS[u] = tS0; S.tagZ[u] = tZ0; }
       bar_arrive_n(1 + j, NT);                                 // FULL(j)
     }
     return;
@@ -501,16 +558,9 @@ __global__ void __launch_bounds__(32 * (1 + pc_spl(L))) spmv_pcrow(PartView P, X
   for (int c = 0; c < nch; ++c) {
     const int j = c & 1;
     bar_sync_n(1 + j, NT);                                     // FULL(j)
-    MP<L> t[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-#pragma unroll
-      for (int k = 0; k < L; ++k) t[u].m[k] = slot[j][k][u][lane];
-      t[u].e = (int32_t)slot[j][L][u][lane];
-      t[u].s = slot[j][L + 1][u][lane];
-    }
+    consume_slot<L, U>(ch, slot[j], lane);
+    if (lane == 0) { pub[0] = ch.E; pub[1] = (int32_t)ch.sg; pub[2] = ch.szero ? 1 : 0; }
     if (c + 2 < nch) bar_arrive_n(3 + j, NT);                  // EMPTY(j)
-    consume_u<L, U>(ch, t, lane);
   }
   MP<L> s;
   ch.exact(s);
@@ -532,7 +582,16 @@ static int launch_wrow_L(const PartView& P, const XView& x, const YView& y, cuda
 template <int L>
 static int launch_pcrow_L(const PartView& P, const XView& x, const YView& y, cudaStream_t st) {
   if (P.npcrow <= 0) return 0;
-  spmv_pcrow<L><<<(unsigned)P.npcrow, 32 * (1 + pc_spl(L)), 0, st>>>(P, x, y);
+  constexpr int U = pc_spl(L);
+  const size_t smem = 2 * sizeof(PcSlot<L, U>) + 16;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(spmv_pcrow<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    attr = true;
+  }
+  spmv_pcrow<L><<<(unsigned)P.npcrow, 32 * (1 + U), smem, st>>>(P, x, y);
   launch_counter_add(1);
   return (int)cudaGetLastError();
 }
