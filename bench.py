@@ -382,6 +382,12 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks,
         "imad_bench": ib,
+        "paper_context": {
+            "value": 1.79e6, "unit": "MP-nnz/s (lower bound, derived)",
+            "note": "arXiv 1411.2377 reports no SpMV rate; BASELINE.md section 2 derives >= 2 nnz "
+                    "per BiCG iteration time: epb3 (n=84617, nnz=463625), p=2048, Intel Core i7 "
+                    "920, 1 thread, MPFR 3.0.1 (PAPER.md:160-166, 440-444, 463). Context only: "
+                    "other precision, matrix and hardware."},
         "setup_s": {"generate": t_gen, "create": t_create},
     }
     s = json.dumps(line)
