@@ -251,8 +251,8 @@ __device__ __forceinline__ void mp_mul(const uint32_t (&a)[L], int32_t ea, uint3
     uint32_t sh = (~T[L + 2]) >> 31;                 // top product bit clear -> 1
     const uint32_t wmask = (1u << (31u - sh)) - 1u;  // T[2] bits below the round bit
     const uint32_t w1 = T[1] >> 5, w2 = T[2] & wmask;
-    const bool amb = ((w1 | w2) == 0u) || (w1 == 0x07FFFFFFu && w2 == wmask);
-    const bool zero = (a[L - 1] == 0u) || (x[L - 1] == 0u);
+    const bool amb = ((w1 | w2) == 0u) | ((w1 == 0x07FFFFFFu) & (w2 == wmask));
+    const bool zero = (a[L - 1] == 0u) | (x[L - 1] == 0u);
     uint32_t stk = 1u;
     if (amb && !zero) {                              // rare: complete the product
       uint32_t c0, c1, c2;
@@ -369,11 +369,12 @@ template <int L>
 __device__ __forceinline__ void mp_add(MP<L>& s, const MP<L>& t) {
   const bool tz = t.is_zero(), sz = s.is_zero();
   const uint32_t mlt = lt_n<L>(s.m, t.m);               // |M_s| < |M_t|
-  const bool t_big = !tz && (sz || t.e > s.e || (t.e == s.e && mlt));
+  // bitwise (not short-circuit) logic: no branches in the common path
+  const bool t_big = !tz & (sz | (t.e > s.e) | ((t.e == s.e) & (mlt != 0u)));
   const int32_t eb = t_big ? t.e : s.e;
   const int32_t esm = t_big ? s.e : t.e;
   const uint32_t sb = t_big ? t.s : s.s;
-  const uint32_t sub = (t.s != s.s && !tz && !sz) ? 1u : 0u;
+  const uint32_t sub = ((t.s != s.s) & !tz & !sz) ? 1u : 0u;
   uint32_t d = (uint32_t)eb - (uint32_t)esm;            // exact as uint32
   d = (tz || sz) ? 0u : min(d, (uint32_t)(32 * (L + 1)));  // d >= p+2: all sticky
   uint32_t Z[L + 1], Y[L + 1];
