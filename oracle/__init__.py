@@ -8,3 +8,4 @@ from .mpref import (ZERO, rn, mul, add, unpack, unpack_vec, pack_vec, row_chain,
 
 __all__ = ["ZERO", "rn", "mul", "add", "unpack", "unpack_vec", "pack_vec",
            "row_chain", "spmv", "spmv_rows", "spmv_t", "spmv_t_cols", "transpose"]
+from . import krylov  # noqa: E402  (BiCG oracle)
