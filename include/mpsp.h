@@ -162,6 +162,45 @@ int mpsp_csr_info(const mpsp_csr *A, int64_t info[10]);
 /* Number of kernels this library has launched in this process (monotone). */
 int64_t mpsp_launch_count(void);
 
+/* ---- BiCG ------------------------------------------
+ * PAPER.md:249-297 (Fig. 4, BiCG; no preconditioner, K = I) from x_0 = 0, and
+ * PAPER.md:375-380 (stop when ||r_i||_2 <= 1e-20 ||r_0||_2 + 1e-50).  Every
+ * operation is one p-bit round-to-nearest-even operation in the order Fig. 4
+ * writes it (readings c26-c31): a dot product is the ordered chain
+ * s = RN(s + RN(u_k v_k)), k ascending, from +0; "a + beta b" is
+ * RN(a + RN(beta b)); ||v|| = RN(sqrt((v, v))); the constants are RN(10^-20)
+ * and RN(10^-50).  All vectors are DEVICE pointers in the element layout
+ * above; scalars are 1-element vectors.  Asynchronous on cuda_stream except
+ * mpsp_bicg, which synchronises once per iteration (3-int flag read).
+ */
+#define MPSP_BICG_CONVERGED  0
+#define MPSP_BICG_BREAKDOWN  1   /* rho = 0 or (p~, z) = 0 */
+#define MPSP_BICG_MAXITER    2
+
+/* out = (u, v): ordered rounded chain over k = 0..n-1 (one element, device). */
+int mpsp_dot(int p_bits, int64_t n,
+             const uint32_t *u_limbs, const int32_t *u_exps, const uint8_t *u_signs,
+             const uint32_t *v_limbs, const int32_t *v_exps, const uint8_t *v_signs,
+             uint32_t *out_limbs, int32_t *out_exps, uint8_t *out_signs, void *cuda_stream);
+
+/* z_k = RN(y_k + RN(+-alpha x_k)), k = 0..n-1 (negate != 0: minus).  alpha is
+ * a 1-element device vector; z may alias y (element-wise in place). */
+int mpsp_axpy(int p_bits, int64_t n,
+              const uint32_t *a_limbs, const int32_t *a_exps, const uint8_t *a_signs, int negate,
+              const uint32_t *x_limbs, const int32_t *x_exps, const uint8_t *x_signs,
+              const uint32_t *y_limbs, const int32_t *y_exps, const uint8_t *y_signs,
+              uint32_t *z_limbs, int32_t *z_exps, uint8_t *z_signs, void *cuda_stream);
+
+/* Solve A x = b by BiCG.  A: a handle over ALL rows built with
+ * MPSP_WITH_TRANSPOSE, p >= 128 (else MPSP_E_NOTRANS / MPSP_E_ARG /
+ * MPSP_E_PREC).  b, x: device n-vectors (x is overwritten; on breakdown it
+ * holds the last complete iterate).  *iters = completed iterations, *status =
+ * MPSP_BICG_*.  Workspace: 6 n-vectors, allocated and freed per call. */
+int mpsp_bicg(mpsp_csr *A,
+              const uint32_t *b_limbs, const int32_t *b_exps, const uint8_t *b_signs,
+              uint32_t *x_limbs, int32_t *x_exps, uint8_t *x_signs,
+              int max_iter, int *iters, int *status, void *cuda_stream);
+
 /*
  * mpsp_imad_bench - measures the sustained 32x32->64 limb-MAC rate of the
  * current device with the same Comba (product-scanning) instruction pattern

@@ -23,7 +23,9 @@ ERROR_CODES = {v: k for k, v in ERRORS.items()}
 # every symbol include/mpsp.h declares
 SYMBOLS = ("mpsp_csr_create", "mpsp_spmv", "mpsp_spmv_t", "mpsp_spmv_host", "mpsp_spmv_t_host",
            "mpsp_destroy", "mpsp_strerror", "mpsp_last_cuda_error", "mpsp_csr_info",
-           "mpsp_launch_count", "mpsp_imad_bench", "mpsp_supported_precision")
+           "mpsp_launch_count", "mpsp_imad_bench", "mpsp_supported_precision",
+           "mpsp_dot", "mpsp_axpy", "mpsp_bicg")
+BICG_STATUS = {0: "converged", 1: "breakdown", 2: "max_iter"}
 
 
 class MpspError(RuntimeError):
@@ -74,6 +76,12 @@ def lib() -> ctypes.CDLL:
     L.mpsp_imad_bench.restype = I
     L.mpsp_supported_precision.argtypes = [I]
     L.mpsp_supported_precision.restype = I
+    L.mpsp_dot.argtypes = [I, I64] + [P] * 9 + [P]
+    L.mpsp_dot.restype = I
+    L.mpsp_axpy.argtypes = [I, I64, P, P, P, I] + [P] * 9 + [P]
+    L.mpsp_axpy.restype = I
+    L.mpsp_bicg.argtypes = [P, P, P, P, P, P, P, I, ctypes.POINTER(I), ctypes.POINTER(I), P]
+    L.mpsp_bicg.restype = I
     _lib = L
     return L
 

@@ -139,6 +139,22 @@ class CSR:
     def spmv_t_host(self, xl, xe, xs, out=None):
         return self._host(_lib.lib().mpsp_spmv_t_host, xl, xe, xs, out)
 
+    def bicg(self, b: MPVec, max_iter: int, x: MPVec | None = None, stream=None):
+        """Solve A x = b by BiCG (Fig. 4, K = I; mpsp_bicg).  Needs a
+        full-matrix handle built with transpose=True and p >= 128.  Returns
+        (x, iterations, status) with status "converged" | "breakdown" |
+        "max_iter"."""
+        if x is None:
+            x = MPVec.empty(self.n, self.L, device=b.limbs.device)
+        if stream is None:
+            stream = torch.cuda.current_stream(b.limbs.device).cuda_stream
+        it, st = ctypes.c_int(0), ctypes.c_int(0)
+        rc = _lib.lib().mpsp_bicg(self._h, _ptr(b.limbs), _ptr(b.exps), _ptr(b.signs),
+                                  _ptr(x.limbs), _ptr(x.exps), _ptr(x.signs), int(max_iter),
+                                  ctypes.byref(it), ctypes.byref(st), ctypes.c_void_p(stream))
+        _lib.check(rc, "mpsp_bicg")
+        return x, it.value, _lib.BICG_STATUS[st.value]
+
     def close(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
@@ -156,3 +172,36 @@ class CSR:
 
     def __exit__(self, *exc):
         self.close()
+
+
+def _stream(dev, stream):
+    if stream is None:
+        return torch.cuda.current_stream(dev).cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+
+
+def dot(p: int, u: MPVec, v: MPVec, out: MPVec | None = None, stream=None) -> MPVec:
+    """(u, v) as the ordered rounded chain (mpsp_dot); a 1-element MPVec."""
+    L = p // 32
+    if out is None:
+        out = MPVec.empty(1, L, device=u.limbs.device)
+    rc = _lib.lib().mpsp_dot(int(p), u.n, _ptr(u.limbs), _ptr(u.exps), _ptr(u.signs),
+                             _ptr(v.limbs), _ptr(v.exps), _ptr(v.signs), _ptr(out.limbs),
+                             _ptr(out.exps), _ptr(out.signs),
+                             ctypes.c_void_p(_stream(u.limbs.device, stream)))
+    _lib.check(rc, "mpsp_dot")
+    return out
+
+
+def axpy(p: int, alpha: MPVec, x: MPVec, y: MPVec, negate: bool = False,
+         out: MPVec | None = None, stream=None) -> MPVec:
+    """out_k = RN(y_k + RN(+-alpha x_k)) (mpsp_axpy); alpha a 1-element MPVec."""
+    if out is None:
+        out = MPVec.empty(x.n, p // 32, device=x.limbs.device)
+    rc = _lib.lib().mpsp_axpy(int(p), x.n, _ptr(alpha.limbs), _ptr(alpha.exps), _ptr(alpha.signs),
+                              1 if negate else 0, _ptr(x.limbs), _ptr(x.exps), _ptr(x.signs),
+                              _ptr(y.limbs), _ptr(y.exps), _ptr(y.signs), _ptr(out.limbs),
+                              _ptr(out.exps), _ptr(out.signs),
+                              ctypes.c_void_p(_stream(x.limbs.device, stream)))
+    _lib.check(rc, "mpsp_axpy")
+    return out

@@ -58,6 +58,12 @@ struct XView {
   const uint8_t* signs;       // [n]
 };
 
+struct VecIn {                // a read-only MP vector (ABI format)
+  const uint32_t* limbs;
+  const int32_t* exps;
+  const uint8_t* signs;
+};
+
 struct YView {
   uint32_t* limbs;            // [rows * L]
   int32_t* exps;
@@ -76,6 +82,16 @@ int pc_row_threshold();
 int launch_spmv_pc(int L, const PartView& P, const XView& x, const YView& y, void* stream);
 // Launch counter increment (shared by the kernel files).
 void launch_counter_add(int64_t k);
+// BiCG building blocks (krylov.cu); each returns a cudaError_t value.
+// Scalars / flags: the BiCG state arrays of mpsp_api.cpp (enum in krylov.cu).
+int krylov_dot(int L, int64_t n, const VecIn& u, const VecIn& v, const YView& out, const int* stop,
+               void* stream);
+int krylov_axpy(int L, int64_t n, const VecIn& al, int neg, const VecIn& x, const VecIn& y,
+                const YView& z, const int* stop, void* stream);
+int krylov_scalar(int L, const YView& S, int* fl, int op, void* stream);
+enum { KS_RHO, KS_RHOP, KS_SIGMA, KS_ALPHA, KS_BETA, KS_RR, KS_NRM, KS_THR, KS_C1, KS_C2, KS_ONE,
+       KS_T20, KS_T50, KS_N };
+enum { KF_STOP, KF_BREAK, KF_CONV, KF_N };
 // Integer-MAC microbenchmark (roofline denominator); returns cudaError_t.
 int run_imad_bench(double out[3]);
 // Launches this process has made.

@@ -594,6 +594,191 @@ int mpsp_csr_info(const mpsp_csr* A, int64_t info[10]) {
   return MPSP_OK;
 }
 
+// ---------------------------------------------------------------- BiCG
+// PAPER.md:249-297 (Fig. 4, K = I) and 375-380 (parity-tested against the
+// test suite's CPU reference of the same steps).
+namespace {
+
+int check_vec_args(int p_bits, int64_t n, const void* a, const void* b, const void* c) {
+  if (!mpsp_supported_precision(p_bits) || n < 0) return n < 0 ? MPSP_E_ARG : MPSP_E_PREC;
+  if (n > 0 && (!a || !b || !c)) return MPSP_E_ARG;
+  return MPSP_OK;
+}
+
+// exact integer k >= 0 -> ABI limbs/exp/sign at precision p (no rounding: k
+// must fit in p bits, which holds for 1, 10^20 and 10^50 at p >= 128)
+void encode_int(int L, uint32_t* limbs, int32_t* e, uint8_t* s, const std::vector<uint32_t>& mag) {
+  // mag: little-endian 32-bit words of k
+  int top = (int)mag.size() - 1;
+  while (top >= 0 && mag[(size_t)top] == 0u) --top;
+  for (int i = 0; i < L; ++i) limbs[i] = 0u;
+  *e = 0; *s = 0;
+  if (top < 0) return;
+  const int bl = 32 * top + 32 - __builtin_clz(mag[(size_t)top]);
+  const int sh = 32 * L - bl;                         // left shift into the mantissa
+  for (int i = 0; i <= top; ++i) {
+    const uint64_t v = (uint64_t)mag[(size_t)i];
+    const int pos = 32 * i + sh;
+    const int w = pos / 32, b = pos % 32;
+    if (w < L) limbs[w] |= (uint32_t)(v << b);
+    if (b && w + 1 < L) limbs[w + 1] |= (uint32_t)(v >> (32 - b));
+  }
+  *e = bl;
+}
+
+std::vector<uint32_t> pow10_words(int k) {
+  std::vector<uint32_t> m{1u};
+  for (int i = 0; i < k; ++i) {
+    uint64_t c = 0;
+    for (auto& w : m) {
+      const uint64_t t = (uint64_t)w * 10u + c;
+      w = (uint32_t)t;
+      c = t >> 32;
+    }
+    if (c) m.push_back((uint32_t)c);
+  }
+  return m;
+}
+
+}  // namespace
+
+int mpsp_dot(int p_bits, int64_t n, const uint32_t* u_limbs, const int32_t* u_exps,
+             const uint8_t* u_signs, const uint32_t* v_limbs, const int32_t* v_exps,
+             const uint8_t* v_signs, uint32_t* out_limbs, int32_t* out_exps, uint8_t* out_signs,
+             void* cuda_stream) {
+  int rc = check_vec_args(p_bits, n, u_limbs, v_limbs, out_limbs);
+  if (rc) return rc;
+  if (!out_limbs || !out_exps || !out_signs) return MPSP_E_ARG;
+  const int L = p_bits / 32;
+  VecIn u{u_limbs, u_exps, u_signs}, v{v_limbs, v_exps, v_signs};
+  YView o{out_limbs, out_exps, out_signs};
+  const int e = krylov_dot(L, n, u, v, o, nullptr, cuda_stream);
+  return e ? cuda_fail((cudaError_t)e) : MPSP_OK;
+}
+
+int mpsp_axpy(int p_bits, int64_t n, const uint32_t* a_limbs, const int32_t* a_exps,
+              const uint8_t* a_signs, int negate, const uint32_t* x_limbs, const int32_t* x_exps,
+              const uint8_t* x_signs, const uint32_t* y_limbs, const int32_t* y_exps,
+              const uint8_t* y_signs, uint32_t* z_limbs, int32_t* z_exps, uint8_t* z_signs,
+              void* cuda_stream) {
+  int rc = check_vec_args(p_bits, n, x_limbs, y_limbs, z_limbs);
+  if (rc) return rc;
+  if (!a_limbs || !a_exps || !a_signs) return MPSP_E_ARG;
+  const int L = p_bits / 32;
+  VecIn a{a_limbs, a_exps, a_signs}, x{x_limbs, x_exps, x_signs}, y{y_limbs, y_exps, y_signs};
+  YView z{z_limbs, z_exps, z_signs};
+  const int e = krylov_axpy(L, n, a, negate ? 1 : 0, x, y, z, nullptr, cuda_stream);
+  return e ? cuda_fail((cudaError_t)e) : MPSP_OK;
+}
+
+int mpsp_bicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, const uint8_t* b_signs,
+              uint32_t* x_limbs, int32_t* x_exps, uint8_t* x_signs, int max_iter, int* iters,
+              int* status, void* cuda_stream) {
+  if (!A || !iters || !status || max_iter < 0) return MPSP_E_ARG;
+  if (!A->has_t) return MPSP_E_NOTRANS;
+  if (A->rb != 0 || A->re != A->n) return MPSP_E_ARG;   // needs the whole matrix
+  if (A->p < 128) return MPSP_E_PREC;                     // 10^50 exact in p bits
+  const int L = A->L;
+  const int64_t n = A->n;
+  *iters = 0;
+  *status = MPSP_BICG_MAXITER;
+  if (n > 0 && (!b_limbs || !b_exps || !b_signs || !x_limbs || !x_exps || !x_signs)) return MPSP_E_ARG;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  cudaError_t ce;
+  // workspace: r, rt, p, pt, z, zt (ABI vectors), KS_N scalars, KF_N flags
+  const size_t vl = (size_t)n * L * 4, ve = (size_t)n * 4, vs = (size_t)n;
+  auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  const size_t per = al(vl) + al(ve) + al(vs);
+  const size_t sbytes = al((size_t)KS_N * L * 4) + al((size_t)KS_N * 4) + al(KS_N) + 256;
+  char* ws = nullptr;
+  if ((ce = cudaMalloc(&ws, 6 * per + sbytes)) != cudaSuccess) { cudaGetLastError(); return MPSP_E_NOMEM; }
+  struct V { uint32_t* l; int32_t* e; uint8_t* s; };
+  V vec[6];
+  for (int i = 0; i < 6; ++i) {
+    char* b0 = ws + i * per;
+    vec[i] = V{(uint32_t*)b0, (int32_t*)(b0 + al(vl)), (uint8_t*)(b0 + al(vl) + al(ve))};
+  }
+  char* sb = ws + 6 * per;
+  YView S{(uint32_t*)sb, (int32_t*)(sb + al((size_t)KS_N * L * 4)),
+          (uint8_t*)(sb + al((size_t)KS_N * L * 4) + al((size_t)KS_N * 4))};
+  int* fl = (int*)(sb + al((size_t)KS_N * L * 4) + al((size_t)KS_N * 4) + al(KS_N));
+  V &r = vec[0], &rt = vec[1], &pv = vec[2], &pt = vec[3], &z = vec[4], &zt = vec[5];
+  auto in = [](const V& v) { return VecIn{v.l, v.e, v.s}; };
+  auto out = [](const V& v) { return YView{v.l, v.e, v.s}; };
+  auto sc_in = [&](int i) { return VecIn{S.limbs + (size_t)i * L, S.exps + i, S.signs + i}; };
+  auto sc_out = [&](int i) { return YView{S.limbs + (size_t)i * L, S.exps + i, S.signs + i}; };
+  int rc = MPSP_OK;
+  auto K = [&](int e) { if (e && rc == MPSP_OK) rc = cuda_fail((cudaError_t)e); };
+  auto cp = [&](const V& src, const V& dst) {
+    if (n == 0) return;
+    K((int)cudaMemcpyAsync(dst.l, src.l, vl, cudaMemcpyDeviceToDevice, st));
+    K((int)cudaMemcpyAsync(dst.e, src.e, ve, cudaMemcpyDeviceToDevice, st));
+    K((int)cudaMemcpyAsync(dst.s, src.s, vs, cudaMemcpyDeviceToDevice, st));
+  };
+  // constants 1, 10^20, 10^50 (exact integers) and flags
+  {
+    std::vector<uint32_t> hl((size_t)KS_N * L, 0u);
+    std::vector<int32_t> he(KS_N, 0);
+    std::vector<uint8_t> hs(KS_N, 0);
+    encode_int(L, &hl[(size_t)KS_ONE * L], &he[KS_ONE], &hs[KS_ONE], {1u});
+    encode_int(L, &hl[(size_t)KS_T20 * L], &he[KS_T20], &hs[KS_T20], pow10_words(20));
+    encode_int(L, &hl[(size_t)KS_T50 * L], &he[KS_T50], &hs[KS_T50], pow10_words(50));
+    K((int)cudaMemcpyAsync(S.limbs, hl.data(), hl.size() * 4, cudaMemcpyHostToDevice, st));
+    K((int)cudaMemcpyAsync(S.exps, he.data(), he.size() * 4, cudaMemcpyHostToDevice, st));
+    K((int)cudaMemcpyAsync(S.signs, hs.data(), hs.size(), cudaMemcpyHostToDevice, st));
+    K((int)cudaMemsetAsync(fl, 0, KF_N * sizeof(int), st));
+    // synchronous: the host vectors above must outlive the copies
+    K((int)cudaStreamSynchronize(st));
+  }
+  // x_0 = 0, r_0 = b, r~_0 = r_0
+  if (n > 0) {
+    K((int)cudaMemsetAsync(x_limbs, 0, vl, st));
+    K((int)cudaMemsetAsync(x_exps, 0, ve, st));
+    K((int)cudaMemsetAsync(x_signs, 0, vs, st));
+  }
+  V bv{(uint32_t*)b_limbs, (int32_t*)b_exps, (uint8_t*)b_signs};
+  V xv{x_limbs, x_exps, x_signs};
+  cp(bv, r);
+  cp(bv, rt);
+  K(krylov_dot(L, n, in(r), in(r), sc_out(KS_RR), fl, st));
+  K(krylov_scalar(L, S, fl, 0, st));
+  int hfl[KF_N] = {0, 0, 0};
+  for (int i = 1; i <= max_iter && rc == MPSP_OK; ++i) {
+    K(krylov_dot(L, n, in(rt), in(r), sc_out(KS_RHO), fl, st));
+    K(krylov_scalar(L, S, fl, 1, st));                       // rho == 0 -> stop
+    if (i == 1) {
+      cp(r, pv);
+      cp(rt, pt);
+    } else {
+      K(krylov_scalar(L, S, fl, 2, st));                     // beta
+      K(krylov_axpy(L, n, sc_in(KS_BETA), 0, in(pv), in(r), out(pv), fl, st));
+      K(krylov_axpy(L, n, sc_in(KS_BETA), 0, in(pt), in(rt), out(pt), fl, st));
+    }
+    for (int tr = 0; tr < 2 && rc == MPSP_OK; ++tr) {          // z = A p, z~ = A^T p~
+      const V& src = tr ? pt : pv;
+      const V& dst = tr ? zt : z;
+      const int e = do_spmv(A, tr == 1, src.l, src.e, src.s, dst.l, dst.e, dst.s, cuda_stream, false);
+      if (e != MPSP_OK) rc = e;
+    }
+    K(krylov_dot(L, n, in(pt), in(z), sc_out(KS_SIGMA), fl, st));
+    K(krylov_scalar(L, S, fl, 3, st));                       // alpha (sigma == 0 -> stop)
+    K(krylov_axpy(L, n, sc_in(KS_ALPHA), 0, in(pv), in(xv), out(xv), fl, st));
+    K(krylov_axpy(L, n, sc_in(KS_ALPHA), 1, in(z), in(r), out(r), fl, st));
+    K(krylov_axpy(L, n, sc_in(KS_ALPHA), 1, in(zt), in(rt), out(rt), fl, st));
+    K(krylov_dot(L, n, in(r), in(r), sc_out(KS_RR), fl, st));
+    K(krylov_scalar(L, S, fl, 4, st));                       // ||r|| <= thr -> stop
+    K((int)cudaMemcpyAsync(hfl, fl, sizeof hfl, cudaMemcpyDeviceToHost, st));
+    K((int)cudaStreamSynchronize(st));
+    if (rc != MPSP_OK) break;
+    if (hfl[KF_BREAK]) { *status = MPSP_BICG_BREAKDOWN; break; }
+    *iters = i;
+    if (hfl[KF_CONV]) { *status = MPSP_BICG_CONVERGED; break; }
+  }
+  cudaStreamSynchronize(st);
+  cudaFree(ws);
+  return rc;
+}
+
 int mpsp_imad_bench(double out[3]) {
   if (!out) return MPSP_E_ARG;
   int e = run_imad_bench(out);

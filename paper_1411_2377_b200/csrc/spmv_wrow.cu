@@ -31,6 +31,7 @@
 #include <cstdlib>
 
 #include "kernel_common.cuh"
+#include "wchain.cuh"
 
 namespace mpsp {
 
@@ -46,33 +47,6 @@ int long_row_threshold() {
 int pc_row_threshold() {
   const char* v = std::getenv("MPSP_PC_T");
   return v ? std::atoi(v) : INT_MAX;                 // opt-in (no faster yet)
-}
-
-// High-part scale H = 2^(p-HB) grid units: S/H in [2^(HB-1), 2^HB).  HB = 26
-// keeps the 32-lane scan of |h| <= 2^25 (plus Shi and the error count) in
-// int32; one unit of H is >= one grid unit u for every p >= 32.
-constexpr int HB = 26;
-
-template <int L>
-__device__ __forceinline__ int32_t hi_of_mant(const uint32_t (&m)[L]) {
-  return (int32_t)(m[L - 1] >> (32 - HB));
-}
-
-// floor(Q / H) for an (L+2)-limb two's complement Q with |Q| <= 2^(p-1) + 1
-template <int L>
-__device__ __forceinline__ int32_t hi_of_q(const uint32_t (&Q)[L + 2]) {
-  return (int32_t)__funnelshift_r(Q[L - 1], Q[L], 32 - HB);
-}
-
-template <int N>
-__device__ __forceinline__ void warp_sum_limbs(uint32_t (&S)[N]) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    uint32_t T[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) T[i] = __shfl_xor_sync(0xffffffffu, S[i], o);
-    add_n<N>(S, S, T);
-  }
 }
 
 template <int L>
@@ -110,144 +84,6 @@ __device__ __forceinline__ void wload(const PartView& P, const XView& x, int64_t
 __device__ __forceinline__ int wcol(const PartView& P, int64_t e0, int jb, int len, int lane) {
   return (jb + lane < len) ? __ldg(P.col + e0 + jb + lane) : 0;
 }
-
-// The chain state of one row held by one warp, and the exact block sum.
-template <int L>
-struct WChain {
-  static constexpr int N = L + 2;
-  uint32_t R[N];          // this lane's share of S (two's complement)
-  bool szero;             // accumulator is exactly zero (warp-uniform)
-  int32_t E;              // accumulator exponent (warp-uniform)
-  uint32_t sg;            // accumulator sign
-  int32_t Shi, err;       // S/H in [Shi, Shi + err)
-
-  __device__ __forceinline__ void init() {
-#pragma unroll
-    for (int i = 0; i < N; ++i) R[i] = 0u;
-    szero = true;
-    E = 0;
-    sg = 0u;
-    Shi = 0;
-    err = 0;
-  }
-
-  __device__ __forceinline__ void reset_to(const MP<L>& s, int lane) {
-    szero = s.is_zero();
-#pragma unroll
-    for (int i = 0; i < N; ++i) R[i] = (lane == 0 && i < L) ? s.m[i] : 0u;
-    E = s.e;
-    sg = s.s;
-    Shi = szero ? 0 : hi_of_mant<L>(s.m);
-    err = 1;
-  }
-
-  // exact S (all lanes)
-  __device__ __forceinline__ void exact(MP<L>& s) const {
-    uint32_t S[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) S[i] = R[i];
-    warp_sum_limbs<N>(S);
-#pragma unroll
-    for (int i = 0; i < L; ++i) s.m[i] = szero ? 0u : S[i];
-    s.e = E;
-    s.s = sg;
-  }
-
-  // s := the chain over this warp's 32 products t (lane k holds step k)
-  __device__ __forceinline__ void consume(const MP<L>& t, int lane) {
-    constexpr unsigned FULL = 0xffffffffu;
-    constexpr int32_t LO = 1 << (HB - 1), HI = 1 << HB;
-    const unsigned below = (1u << lane) - 1u;
-    const bool tz = t.is_zero();       // padding lanes have zero limbs
-    int start = 0;
-    while (start < 32) {
-      if (szero) {
-        // s = +0: the first nonzero product is absorbed exactly
-        const unsigned nzm = __ballot_sync(FULL, !tz && lane >= start);
-        if (nzm == 0u) break;
-        const int f = __ffs(nzm) - 1;
-        MP<L> tf;
-#pragma unroll
-        for (int i = 0; i < L; ++i) tf.m[i] = __shfl_sync(FULL, t.m[i], f);
-        tf.e = __shfl_sync(FULL, t.e, f);
-        tf.s = __shfl_sync(FULL, t.s, f);
-        reset_to(tf, lane);
-        start = f + 1;
-        continue;
-      }
-      const bool act = (lane >= start) && !tz;
-      const int64_t d64 = (int64_t)E - (int64_t)t.e;
-      const bool badd = act && d64 < 1;              // |t| >= 2^(E-1): leaves the binade
-      const bool use = act && !badd;
-      const uint32_t dd = use ? (uint32_t)min(d64, (int64_t)(32 * L + 32)) : 0u;
-      // Y = |t| / u  as integer limbs Y[1..L] and guard limb Y[0]
-      uint32_t Y[L + 1];
-      Y[0] = 0u;
-#pragma unroll
-      for (int i = 0; i < L; ++i) Y[i + 1] = t.m[i];
-      uint32_t stk = 0u;
-      shr_bits_sticky<L + 1>(Y, dd, stk);
-      const uint32_t rb = Y[0] >> 31;
-      const bool sticky = (stk | (Y[0] << 1)) != 0u;
-      const bool tie = use && rb && !sticky;
-      uint32_t inc = (rb && sticky) ? 1u : 0u;
-      const uint32_t lsbY = Y[1] & 1u;
-      const unsigned tieM = __ballot_sync(FULL, tie);
-      if (tieM) {                                     // warp-uniform, rare
-        // parity of S_{k-1}: that of S (XOR of the lanes' R low bits), reset
-        // to 0 by the last tie before k, XORed with the non-tie Q_j low bits
-        const uint32_t par = (uint32_t)__popc(__ballot_sync(FULL, R[0] & 1u)) & 1u;
-        const unsigned bM = __ballot_sync(FULL, use && !tie && ((lsbY ^ inc) & 1u));
-        if (tie) {
-          const unsigned tb = tieM & below;
-          const int lt = tb ? 31 - __clz(tb) : -1;
-          const unsigned seg = below & (lt >= 0 ? ~((2u << lt) - 1u) : FULL);
-          const uint32_t pS = ((lt >= 0 ? 0u : par) ^ (uint32_t)__popc(bM & seg)) & 1u;
-          inc = pS ^ lsbY;                            // make S_k even
-        }
-      }
-      // Q = +-(Y + inc) in N-limb two's complement, one carry chain:
-      // -(Y + inc) = ~Y + (1 - inc)
-      const uint32_t neg = (use && t.s != sg) ? 1u : 0u;
-      const uint32_t nm = 0u - neg;
-      uint32_t Q[N];
-#pragma unroll
-      for (int i = 0; i < L; ++i) Q[i] = (use ? Y[i + 1] : 0u) ^ nm;
-      Q[L] = nm;
-      Q[L + 1] = nm;
-      inc_n<N>(Q, use ? (neg ? 1u - inc : inc) : 0u);
-      const int32_t h = hi_of_q<L>(Q);
-      int32_t Pi = h;                                 // inclusive scan of h
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int32_t v = __shfl_up_sync(FULL, Pi, o);
-        if (lane >= o) Pi += v;
-      }
-      const int32_t LB = Shi + (Pi - h);              // S_{k-1}/H >= LB
-      const int32_t ek = err + lane;                  // S_{k-1}/H < LB + ek
-      const bool ok = !act || (!badd && LB + h - 1 >= LO && LB + ek + h + 1 <= HI);
-      const unsigned failM = __ballot_sync(FULL, !ok);
-      if (failM == 0u) {
-        add_n<N>(R, R, Q);
-        Shi += __shfl_sync(FULL, Pi, 31);
-        err = min(err + 32, 1 << 28);                 // saturates: checks then fail
-        break;
-      }
-      // ---- exact path at the first failing step f
-      const int f = __ffs(failM) - 1;
-      if (lane < f) add_n<N>(R, R, Q);               // steps before f are valid
-      MP<L> s, tf;
-      exact(s);
-#pragma unroll
-      for (int i = 0; i < L; ++i) tf.m[i] = __shfl_sync(FULL, t.m[i], f);
-      tf.e = __shfl_sync(FULL, t.e, f);
-      tf.s = __shfl_sync(FULL, t.s, f);
-      mp_add<L>(s, tf);
-      reset_to(s, lane);
-      start = f + 1;
-    }
-  }
-};
 
 #ifndef MPSP_WROW_MINB
 #define MPSP_WROW_MINB 1
