@@ -13,6 +13,7 @@
 // nothing, so x keeps the last complete iterate, as in the oracle).
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdint>
 #include <cstring>
 #include <vector>
@@ -59,6 +60,219 @@ __global__ void __launch_bounds__(32) vec_dot(int64_t n, VecIn u, VecIn v, YView
   MP<L> s;
   ch.exact(s);
   if (lane == 0) store_y<L>(out, 0, s);
+}
+
+// ---------------------------------------------------------------------------
+// Fast exact dot: the chain split into segments of DSEG steps, evaluated
+// speculatively in parallel and validated in order.
+//  D1 (warp per segment): products t_k into a scratch array, and an fp64
+//     estimate of the segment's sum;
+//  D2 (warp per segment s >= 1): the accumulator's binade E_g and sign at the
+//     segment start are GUESSED from the fp64 prefix sum; every step's grid
+//     increment Q_k against (E_g, sign) is formed (align_q), summed exactly
+//     (dS), and the relative high-part prefix bounds of the segment's partial
+//     sums (minv, maxv) recorded; a tie or a step reaching the binade makes
+//     the segment invalid;
+//  D3 (one warp): the chain itself (WChain) walks the segments in order: a
+//     segment whose guess matches the exact state (E, sign) and whose bounds
+//     hold for the exact Shi / err is committed by adding dS (32 segments
+//     validated per warp step, by scans of the segments' h sums and step
+//     counts); any other segment is evaluated step by step from the stored
+//     products.  Validation uses exactly the conditions WChain::consume
+//     checks block by block, so the result is the ordered chain's, bit for bit.
+// ---------------------------------------------------------------------------
+constexpr int DSEG_NB = 8;                       // blocks of 32 steps per segment
+constexpr int DSEG = 32 * DSEG_NB;
+
+struct DotWork {                                  // device scratch (sizes: dot_work_bytes)
+  uint32_t* prod;                                 // [nblk][L+2][32] products
+  double* segsum;                                 // [nseg]
+  int32_t* valid;                                 // [nseg]
+  int32_t* eg;                                    // [nseg]
+  uint32_t* sg;                                   // [nseg]
+  long long* minv;                                // [nseg]
+  long long* maxv;                                // [nseg]
+  long long* htot;                                // [nseg]
+  uint32_t* ds;                                    // [nseg][L+2] exact segment sums
+};
+
+template <int L>
+__device__ __forceinline__ double mp_to_f64(const MP<L>& t) {
+  if (t.is_zero()) return 0.0;
+  const unsigned long long top = ((unsigned long long)t.m[L - 1] << 32) | (L > 1 ? t.m[L > 1 ? L - 2 : 0] : 0u);
+  const double d = ldexp(__ull2double_rn(top), t.e - 64);
+  return t.s ? -d : d;
+}
+
+template <int L>
+__global__ void __launch_bounds__(128) dot_products(int64_t n, VecIn u, VecIn v, DotWork W,
+                                                    int64_t nseg, const int* stop) {
+  if (stop && *stop) return;
+  const int64_t seg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (seg >= nseg) return;
+  double acc = 0.0;
+  for (int b = 0; b < DSEG_NB; ++b) {
+    const int64_t blk = seg * DSEG_NB + b;
+    const int64_t k = blk * 32 + lane;
+    MP<L> t;
+    if (k < n) {
+      MP<L> a, c;
+      load_mp<L>(u, k, a);
+      load_mp<L>(v, k, c);
+      mp_mul<L>(a.m, a.e, a.s, c.m, c.e, c.s, t);
+    } else {
+      t.set_zero();
+    }
+    uint32_t* P = W.prod + blk * (L + 2) * 32;
+#pragma unroll
+    for (int i = 0; i < L; ++i) P[i * 32 + lane] = t.m[i];
+    P[L * 32 + lane] = (uint32_t)t.e;
+    P[(L + 1) * 32 + lane] = t.s;
+    acc += mp_to_f64<L>(t);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) W.segsum[seg] = acc;
+}
+
+template <int L>
+__device__ __forceinline__ void load_prod(const DotWork& W, int64_t blk, int lane, MP<L>& t) {
+  const uint32_t* P = W.prod + blk * (L + 2) * 32;
+#pragma unroll
+  for (int i = 0; i < L; ++i) t.m[i] = P[i * 32 + lane];
+  t.e = (int32_t)P[L * 32 + lane];
+  t.s = P[(L + 1) * 32 + lane];
+}
+
+template <int L>
+__global__ void __launch_bounds__(128) dot_speculate(DotWork W, int64_t nseg, const int* stop) {
+  if (stop && *stop) return;
+  constexpr int N = L + 2;
+  constexpr unsigned FULL = 0xffffffffu;
+  const int64_t seg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (seg >= nseg || seg == 0) return;
+  double pre = 0.0;                                // fp64 prefix of the segment sums
+  for (int64_t j = lane; j < seg; j += 32) pre += W.segsum[j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(FULL, pre, o);
+  int e2 = 0;
+  const double f = frexp(fabs(pre), &e2);
+  bool valid = (pre != 0.0) && isfinite(pre) && f > 0.0;
+  const int32_t Eg = e2;
+  const uint32_t sgg = pre < 0.0 ? 1u : 0u;
+  uint32_t R[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) R[i] = 0u;
+  long long base = 0, mn = LLONG_MAX, mx = LLONG_MIN;
+  for (int b = 0; b < DSEG_NB && valid; ++b) {
+    MP<L> t;
+    load_prod<L>(W, seg * DSEG_NB + b, lane, t);
+    const bool act = !t.is_zero();
+    uint32_t Q[N];
+    int32_t h;
+    bool prex;
+    align_q<L>(t, act, Eg, sgg, Q, h, prex);
+    if (__ballot_sync(FULL, act && prex)) valid = false;
+    long long Pi = act ? h : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long x = __shfl_up_sync(FULL, Pi, o);
+      if (lane >= o) Pi += x;
+    }
+    const long long before = base + Pi - (act ? h : 0);
+    long long cmn = act ? before + h : LLONG_MAX;
+    long long cmx = act ? before + h + b * 32 + lane : LLONG_MIN;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      cmn = min(cmn, (long long)__shfl_xor_sync(FULL, cmn, o));
+      cmx = max(cmx, (long long)__shfl_xor_sync(FULL, cmx, o));
+    }
+    mn = min(mn, cmn);
+    mx = max(mx, cmx);
+    add_n<N>(R, R, Q);
+    base += __shfl_sync(FULL, Pi, 31);
+  }
+  warp_sum_limbs<N>(R);
+  if (lane == 0) {
+    W.valid[seg] = valid ? 1 : 0;
+    W.eg[seg] = Eg;
+    W.sg[seg] = sgg;
+    W.minv[seg] = mn;
+    W.maxv[seg] = mx;
+    W.htot[seg] = base;
+  }
+  if (lane < N) {
+    uint32_t v = R[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i) v = (lane == i) ? R[i] : v;
+    W.ds[seg * N + lane] = v;
+  }
+}
+
+template <int L>
+__global__ void __launch_bounds__(32) dot_chain(int64_t n, DotWork W, int64_t nseg, YView out,
+                                                const int* stop) {
+  if (stop && *stop) return;
+  constexpr int N = L + 2;
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr long long LO = 1ll << (HB - 1), HI = 1ll << HB;
+  const int lane = threadIdx.x & 31;
+  WChain<L> ch;
+  ch.init();
+  auto sequential = [&](int64_t seg) {
+    for (int b = 0; b < DSEG_NB; ++b) {
+      const int64_t blk = seg * DSEG_NB + b;
+      if (blk * 32 >= n) break;
+      MP<L> t;
+      load_prod<L>(W, blk, lane, t);
+      ch.consume(t, lane);
+    }
+  };
+  int64_t s = 0;
+  while (s < nseg) {
+    if (s == 0 || ch.szero) {
+      sequential(s);
+      ++s;
+      continue;
+    }
+    const int64_t j = s + lane;
+    const bool in = j < nseg;
+    const long long ht = in ? W.htot[j] : 0;
+    const long long cn = DSEG;
+    long long hi = ht, ci = cn;                     // inclusive scans
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long x = __shfl_up_sync(FULL, hi, o);
+      const long long y = __shfl_up_sync(FULL, ci, o);
+      if (lane >= o) { hi += x; ci += y; }
+    }
+    const long long hpre = hi - ht, cpre = ci - cn;
+    bool ok = in && W.valid[j] && W.eg[j] == ch.E && W.sg[j] == ch.sg;
+    ok = ok && ((long long)ch.Shi + hpre + W.minv[j] - 1 >= LO) &&
+         ((long long)ch.Shi + hpre + (long long)ch.err + cpre + W.maxv[j] + 1 <= HI);
+    const unsigned failM = __ballot_sync(FULL, !ok);
+    const int f = failM ? __ffs(failM) - 1 : 32;
+    if (f > 0) {
+      if (lane < f) {
+        uint32_t D[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) D[i] = W.ds[j * N + i];
+        add_n<N>(ch.R, ch.R, D);
+      }
+      ch.Shi = (int32_t)((long long)ch.Shi + __shfl_sync(FULL, hi, f - 1));
+      ch.err = (int32_t)min((long long)ch.err + __shfl_sync(FULL, ci, f - 1), 1ll << 28);
+      s += f;
+    }
+    if (f < 32 && s < nseg) {
+      sequential(s);
+      ++s;
+    }
+  }
+  MP<L> r;
+  ch.exact(r);
+  if (lane == 0) store_y<L>(out, 0, r);
 }
 
 template <int L>
@@ -262,10 +476,47 @@ __global__ void bicg_scalar(YView S, int* fl, int op) {
 // ---------------------------------------------------------------- launchers
 template <int L>
 struct KrylovOps {
-  static int dot(int64_t n, VecIn u, VecIn v, YView out, const int* stop, cudaStream_t st) {
-    vec_dot<L><<<1, 32, 0, st>>>(n, u, v, out, stop);
-    launch_counter_add(1);
+  static int dot(int64_t n, VecIn u, VecIn v, YView out, const int* stop, cudaStream_t st,
+                 void* work) {
+    const int64_t nseg = (n + DSEG - 1) / DSEG;
+    if (!work || nseg <= 1) {                      // short vectors: one warp
+      vec_dot<L><<<1, 32, 0, st>>>(n, u, v, out, stop);
+      launch_counter_add(1);
+      return (int)cudaGetLastError();
+    }
+    DotWork W = carve(work, nseg);
+    const unsigned nb = (unsigned)((nseg * 32 + 127) / 128);
+    dot_products<L><<<nb, 128, 0, st>>>(n, u, v, W, nseg, stop);
+    dot_speculate<L><<<nb, 128, 0, st>>>(W, nseg, stop);
+    dot_chain<L><<<1, 32, 0, st>>>(n, W, nseg, out, stop);
+    launch_counter_add(3);
     return (int)cudaGetLastError();
+  }
+  static size_t bytes(int64_t n) {
+    const int64_t nseg = (n + DSEG - 1) / DSEG;
+    return carve_bytes(nseg);
+  }
+  static size_t carve_bytes(int64_t nseg) {
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t nblk = (size_t)nseg * DSEG_NB;
+    return al(nblk * (L + 2) * 32 * 4) + al(nseg * 8) + 3 * al(nseg * 4) + 3 * al(nseg * 8) +
+           al((size_t)nseg * (L + 2) * 4);
+  }
+  static DotWork carve(void* work, int64_t nseg) {
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    char* p = (char*)work;
+    const size_t nblk = (size_t)nseg * DSEG_NB;
+    DotWork W;
+    W.prod = (uint32_t*)p; p += al(nblk * (L + 2) * 32 * 4);
+    W.segsum = (double*)p; p += al(nseg * 8);
+    W.valid = (int32_t*)p; p += al(nseg * 4);
+    W.eg = (int32_t*)p; p += al(nseg * 4);
+    W.sg = (uint32_t*)p; p += al(nseg * 4);
+    W.minv = (long long*)p; p += al(nseg * 8);
+    W.maxv = (long long*)p; p += al(nseg * 8);
+    W.htot = (long long*)p; p += al(nseg * 8);
+    W.ds = (uint32_t*)p;
+    return W;
   }
   static int axpy(int64_t n, VecIn al, int neg, VecIn x, VecIn y, YView z, const int* stop,
                   cudaStream_t st) {
@@ -282,16 +533,28 @@ struct KrylovOps {
 };
 
 int krylov_dot(int L, int64_t n, const VecIn& u, const VecIn& v, const YView& out, const int* stop,
-               void* stream) {
+               void* stream, void* work) {
   cudaStream_t st = (cudaStream_t)stream;
   switch (L) {
-    case 1: return KrylovOps<1>::dot(n, u, v, out, stop, st);
-    case 2: return KrylovOps<2>::dot(n, u, v, out, stop, st);
-    case 4: return KrylovOps<4>::dot(n, u, v, out, stop, st);
-    case 8: return KrylovOps<8>::dot(n, u, v, out, stop, st);
-    case 16: return KrylovOps<16>::dot(n, u, v, out, stop, st);
-    case 32: return KrylovOps<32>::dot(n, u, v, out, stop, st);
+    case 1: return KrylovOps<1>::dot(n, u, v, out, stop, st, work);
+    case 2: return KrylovOps<2>::dot(n, u, v, out, stop, st, work);
+    case 4: return KrylovOps<4>::dot(n, u, v, out, stop, st, work);
+    case 8: return KrylovOps<8>::dot(n, u, v, out, stop, st, work);
+    case 16: return KrylovOps<16>::dot(n, u, v, out, stop, st, work);
+    case 32: return KrylovOps<32>::dot(n, u, v, out, stop, st, work);
     default: return (int)cudaErrorInvalidValue;
+  }
+}
+
+size_t krylov_dot_work_bytes(int L, int64_t n) {
+  switch (L) {
+    case 1: return KrylovOps<1>::bytes(n);
+    case 2: return KrylovOps<2>::bytes(n);
+    case 4: return KrylovOps<4>::bytes(n);
+    case 8: return KrylovOps<8>::bytes(n);
+    case 16: return KrylovOps<16>::bytes(n);
+    case 32: return KrylovOps<32>::bytes(n);
+    default: return 0;
   }
 }
 

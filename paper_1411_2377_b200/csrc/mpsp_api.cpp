@@ -652,7 +652,13 @@ int mpsp_dot(int p_bits, int64_t n, const uint32_t* u_limbs, const int32_t* u_ex
   const int L = p_bits / 32;
   VecIn u{u_limbs, u_exps, u_signs}, v{v_limbs, v_exps, v_signs};
   YView o{out_limbs, out_exps, out_signs};
-  const int e = krylov_dot(L, n, u, v, o, nullptr, cuda_stream);
+  // segmented parallel evaluation needs a scratch buffer (stream-ordered)
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  void* work = nullptr;
+  const size_t wb = krylov_dot_work_bytes(L, n);
+  if (wb && cudaMallocAsync(&work, wb, st) != cudaSuccess) { cudaGetLastError(); return MPSP_E_NOMEM; }
+  const int e = krylov_dot(L, n, u, v, o, nullptr, cuda_stream, work);
+  if (work) cudaFreeAsync(work, st);
   return e ? cuda_fail((cudaError_t)e) : MPSP_OK;
 }
 
@@ -690,8 +696,10 @@ int mpsp_bicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, const
   auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
   const size_t per = al(vl) + al(ve) + al(vs);
   const size_t sbytes = al((size_t)KS_N * L * 4) + al((size_t)KS_N * 4) + al(KS_N) + 256;
+  const size_t dbytes = al(krylov_dot_work_bytes(L, n));
   char* ws = nullptr;
-  if ((ce = cudaMalloc(&ws, 6 * per + sbytes)) != cudaSuccess) { cudaGetLastError(); return MPSP_E_NOMEM; }
+  if ((ce = cudaMalloc(&ws, 6 * per + sbytes + dbytes)) != cudaSuccess) { cudaGetLastError(); return MPSP_E_NOMEM; }
+  void* dwork = dbytes ? (void*)(ws + 6 * per + sbytes) : nullptr;
   struct V { uint32_t* l; int32_t* e; uint8_t* s; };
   V vec[6];
   for (int i = 0; i < 6; ++i) {
@@ -740,11 +748,11 @@ int mpsp_bicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, const
   V xv{x_limbs, x_exps, x_signs};
   cp(bv, r);
   cp(bv, rt);
-  K(krylov_dot(L, n, in(r), in(r), sc_out(KS_RR), fl, st));
+  K(krylov_dot(L, n, in(r), in(r), sc_out(KS_RR), fl, st, dwork));
   K(krylov_scalar(L, S, fl, 0, st));
   int hfl[KF_N] = {0, 0, 0};
   for (int i = 1; i <= max_iter && rc == MPSP_OK; ++i) {
-    K(krylov_dot(L, n, in(rt), in(r), sc_out(KS_RHO), fl, st));
+    K(krylov_dot(L, n, in(rt), in(r), sc_out(KS_RHO), fl, st, dwork));
     K(krylov_scalar(L, S, fl, 1, st));                       // rho == 0 -> stop
     if (i == 1) {
       cp(r, pv);
@@ -760,12 +768,12 @@ int mpsp_bicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, const
       const int e = do_spmv(A, tr == 1, src.l, src.e, src.s, dst.l, dst.e, dst.s, cuda_stream, false);
       if (e != MPSP_OK) rc = e;
     }
-    K(krylov_dot(L, n, in(pt), in(z), sc_out(KS_SIGMA), fl, st));
+    K(krylov_dot(L, n, in(pt), in(z), sc_out(KS_SIGMA), fl, st, dwork));
     K(krylov_scalar(L, S, fl, 3, st));                       // alpha (sigma == 0 -> stop)
     K(krylov_axpy(L, n, sc_in(KS_ALPHA), 0, in(pv), in(xv), out(xv), fl, st));
     K(krylov_axpy(L, n, sc_in(KS_ALPHA), 1, in(z), in(r), out(r), fl, st));
     K(krylov_axpy(L, n, sc_in(KS_ALPHA), 1, in(zt), in(rt), out(rt), fl, st));
-    K(krylov_dot(L, n, in(r), in(r), sc_out(KS_RR), fl, st));
+    K(krylov_dot(L, n, in(r), in(r), sc_out(KS_RR), fl, st, dwork));
     K(krylov_scalar(L, S, fl, 4, st));                       // ||r|| <= thr -> stop
     K((int)cudaMemcpyAsync(hfl, fl, sizeof hfl, cudaMemcpyDeviceToHost, st));
     K((int)cudaStreamSynchronize(st));

@@ -142,38 +142,6 @@ __global__ void __launch_bounds__(128, (L <= 8 ? MPSP_WROW_MINB : 1)) spmv_wrow(
 // chain 32U steps and the U per-lane alignments are independent (ILP).
 // A tie on the grid is handled as a failing step (exact path).
 // --------------------------------------------------------------------------
-// Grid alignment of one product against the accumulator tag (E, sg): Q =
-// +-RN_int(|t|/u) in (L+2)-limb two's complement, its high part, and whether
-// the step must take the exact path (|t| reaches the binade, or a grid tie).
-template <int L>
-__device__ __forceinline__ void align_q(const MP<L>& t, bool act, int32_t E, uint32_t sg,
-                                        uint32_t (&Q)[L + 2], int32_t& h, bool& pre) {
-  constexpr int N = L + 2;
-  const int64_t d64 = (int64_t)E - (int64_t)t.e;
-  const bool badd = act && d64 < 1;
-  const bool use = act && !badd;
-  const uint32_t dd = use ? (uint32_t)min(d64, (int64_t)(32 * L + 32)) : 0u;
-  uint32_t Y[L + 1];
-  Y[0] = 0u;
-#pragma unroll
-  for (int i = 0; i < L; ++i) Y[i + 1] = t.m[i];
-  uint32_t stk = 0u;
-  shr_bits_sticky<L + 1>(Y, dd, stk);
-  const uint32_t rb = Y[0] >> 31;
-  const bool sticky = (stk | (Y[0] << 1)) != 0u;
-  const bool tie = use && rb && !sticky;
-  const uint32_t inc = (rb && sticky) ? 1u : 0u;
-  pre = badd || tie;
-  const uint32_t neg = (use && t.s != sg) ? 1u : 0u;
-  const uint32_t nm = 0u - neg;
-#pragma unroll
-  for (int i = 0; i < L; ++i) Q[i] = (use ? Y[i + 1] : 0u) ^ nm;
-  Q[L] = nm;
-  Q[L + 1] = nm;
-  inc_n<N>(Q, use ? (neg ? 1u - inc : inc) : 0u);
-  h = hi_of_q<L>(Q);
-}
-
 // Shared-memory chunk of the producer/consumer kernel: per step the raw
 // product and its speculative alignment against the tag the producer read.
 template <int L, int U>

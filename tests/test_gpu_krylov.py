@@ -2,6 +2,8 @@
 (oracle/krylov.py), bit-exact: the ordered-chain dot product, axpy, and whole
 BiCG solves (iterate x, iteration count, status) on diagonally dominant
 banded systems and C1-like random systems, b = A [1..n]^T."""
+import zlib
+
 import numpy as np
 import pytest
 
@@ -146,3 +148,45 @@ def test_bicg_identity_and_errors():
     with pytest.raises(MpspError):
         H.bicg(_vec([K.from_int(1, 64)] * n, 64), 10)   # p >= 128
     H.close()
+
+
+def _dot_case(kind, n, p, rng):
+    L = p // 32
+    if kind == "random":
+        return _rand_vals(rng, n, p, -30, 30, zeros=0.02), _rand_vals(rng, n, p, -30, 30)
+    if kind == "growing":          # running sum's binade keeps changing across segments
+        u = _rand_vals(rng, n, p, 0, 0)
+        u = [(s, M, E + (k * 60) // n) for k, (s, M, E) in enumerate(u)]
+        return u, _rand_vals(rng, n, p, 0, 2)
+    if kind == "cancel":           # exact cancellation back to +0 mid-chain, then restart
+        h = n // 2
+        u = _rand_vals(rng, h, p, -5, 5)
+        v = _rand_vals(rng, h, p, -5, 5)
+        # second half: the negated products of the first half in REVERSE order do not
+        # cancel exactly under rounding; instead repeat the first half with u negated
+        return u + [K.neg(a) for a in u] + _rand_vals(rng, n - 2 * h, p, -5, 5), \
+            v + v + _rand_vals(rng, n - 2 * h, p, -5, 5)
+    if kind == "huge":             # fp64 estimates overflow: every guess invalid
+        u = _rand_vals(rng, n, p, -(1 << 28), 1 << 28)
+        return u, _rand_vals(rng, n, p, -10, 10)
+    if kind == "ties":             # small gaps with 10..0 tails: grid ties everywhere
+        one = K.from_int(1, p)
+        u = [one] + [(rng.integers(0, 2), (1 << (p - 1)) | (1 << int(rng.integers(0, 3))), -p + 2)
+                     for _ in range(n - 1)]
+        return u, [one] * n
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kind", ["random", "growing", "cancel", "huge", "ties"])
+@pytest.mark.parametrize("p,n", [(128, 20000), (256, 60000), (1024, 4000)])
+def test_dot_segmented_paths(kind, p, n):
+    """The segmented speculative dot (n > 256) must equal the ordered chain in
+    every regime: stable binade (segments committed), drifting binade,
+    exact cancellation to +0, fp64-overflowing guesses, grid ties."""
+    import torch
+    from paper_1411_2377_b200.csr import dot
+    rng = np.random.default_rng(zlib.crc32(f"{kind}-{p}-{n}".encode()))
+    u, v = _dot_case(kind, n, p, rng)
+    got = dot(p, _vec(u, p), _vec(v, p))
+    torch.cuda.synchronize()
+    assert_same(got.to_host(), oracle.pack_vec([K.dot(u, v, p)], p), f"dot {kind} p={p} n={n}")
