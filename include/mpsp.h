@@ -201,6 +201,11 @@ int mpsp_bicg(mpsp_csr *A,
               uint32_t *x_limbs, int32_t *x_exps, uint8_t *x_signs,
               int max_iter, int *iters, int *status, void *cuda_stream);
 
+/* Diagnostics of the segmented dot: out[0] = segments the
+ * chain warp evaluated step by step, out[1] = segments committed from their
+ * speculative sums, since the last call (counters are then reset). */
+int mpsp_debug_dot_stats(unsigned long long out[2]);
+
 /*
  * mpsp_imad_bench - measures the sustained 32x32->64 limb-MAC rate of the
  * current device with the same Comba (product-scanning) instruction pattern

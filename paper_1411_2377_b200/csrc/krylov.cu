@@ -211,6 +211,9 @@ __global__ void __launch_bounds__(128) dot_speculate(DotWork W, int64_t nseg, co
   }
 }
 
+// diagnostics: segments evaluated step by step / validated (mpsp_debug_dot_stats)
+__device__ unsigned long long g_dot_stats[2];
+
 template <int L>
 __global__ void __launch_bounds__(32) dot_chain(int64_t n, DotWork W, int64_t nseg, YView out,
                                                 const int* stop) {
@@ -222,6 +225,7 @@ __global__ void __launch_bounds__(32) dot_chain(int64_t n, DotWork W, int64_t ns
   WChain<L> ch;
   ch.init();
   auto sequential = [&](int64_t seg) {
+    if (lane == 0) atomicAdd(&g_dot_stats[0], 1ull);
     for (int b = 0; b < DSEG_NB; ++b) {
       const int64_t blk = seg * DSEG_NB + b;
       if (blk * 32 >= n) break;
@@ -255,6 +259,7 @@ __global__ void __launch_bounds__(32) dot_chain(int64_t n, DotWork W, int64_t ns
     const unsigned failM = __ballot_sync(FULL, !ok);
     const int f = failM ? __ffs(failM) - 1 : 32;
     if (f > 0) {
+      if (lane == 0) atomicAdd(&g_dot_stats[1], (unsigned long long)f);
       if (lane < f) {
         uint32_t D[N];
 #pragma unroll
@@ -544,6 +549,15 @@ int krylov_dot(int L, int64_t n, const VecIn& u, const VecIn& v, const YView& ou
     case 32: return KrylovOps<32>::dot(n, u, v, out, stop, st, work);
     default: return (int)cudaErrorInvalidValue;
   }
+}
+
+int krylov_dot_stats(unsigned long long out[2]) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_dot_stats, sizeof(unsigned long long) * 2);
+  if (e == cudaSuccess) {
+    unsigned long long z[2] = {0ull, 0ull};
+    e = cudaMemcpyToSymbol(g_dot_stats, z, sizeof z);
+  }
+  return (int)e;
 }
 
 size_t krylov_dot_work_bytes(int L, int64_t n) {

@@ -787,6 +787,12 @@ int mpsp_bicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, const
   return rc;
 }
 
+int mpsp_debug_dot_stats(unsigned long long out[2]) {
+  if (!out) return MPSP_E_ARG;
+  const int e = krylov_dot_stats(out);
+  return e ? cuda_fail((cudaError_t)e) : MPSP_OK;
+}
+
 int mpsp_imad_bench(double out[3]) {
   if (!out) return MPSP_E_ARG;
   int e = run_imad_bench(out);

@@ -166,6 +166,9 @@ def _dot_case(kind, n, p, rng):
         # cancel exactly under rounding; instead repeat the first half with u negated
         return u + [K.neg(a) for a in u] + _rand_vals(rng, n - 2 * h, p, -5, 5), \
             v + v + _rand_vals(rng, n - 2 * h, p, -5, 5)
+    if kind == "positive":         # monotone sum: binade changes only ~log2(n) times
+        u = [(0, M, E) for (_, M, E) in _rand_vals(rng, n, p, -8, 8)]
+        return u, [(0, M, E) for (_, M, E) in _rand_vals(rng, n, p, -8, 8)]
     if kind == "huge":             # fp64 estimates overflow: every guess invalid
         u = _rand_vals(rng, n, p, -(1 << 28), 1 << 28)
         return u, _rand_vals(rng, n, p, -10, 10)
@@ -177,7 +180,7 @@ def _dot_case(kind, n, p, rng):
     raise ValueError(kind)
 
 
-@pytest.mark.parametrize("kind", ["random", "growing", "cancel", "huge", "ties"])
+@pytest.mark.parametrize("kind", ["random", "positive", "growing", "cancel", "huge", "ties"])
 @pytest.mark.parametrize("p,n", [(128, 20000), (256, 60000), (1024, 4000)])
 def test_dot_segmented_paths(kind, p, n):
     """The segmented speculative dot (n > 256) must equal the ordered chain in
@@ -186,7 +189,14 @@ def test_dot_segmented_paths(kind, p, n):
     import torch
     from paper_1411_2377_b200.csr import dot
     rng = np.random.default_rng(zlib.crc32(f"{kind}-{p}-{n}".encode()))
+    from paper_1411_2377_b200._lib import dot_stats
     u, v = _dot_case(kind, n, p, rng)
+    dot_stats()
     got = dot(p, _vec(u, p), _vec(v, p))
     torch.cuda.synchronize()
+    st = dot_stats()
     assert_same(got.to_host(), oracle.pack_vec([K.dot(u, v, p)], p), f"dot {kind} p={p} n={n}")
+    if kind == "huge":
+        assert st["validated"] == 0              # overflowing guesses never commit
+    if kind == "positive":
+        assert st["validated"] > st["sequential"]   # the speculative path carries the chain
