@@ -189,3 +189,117 @@ def bicg(p: int, A, b, max_iter: int, trace: bool = False):
             status = "converged"
             break
     return dict(x=x, iters=it, status=status, norms=norms, thr=thr, hist=hist)
+
+
+# --------------------------------------------------------------------------
+# GPBiCG (Fig. 4 right), K = I, over the reals (mu4-bar =
+# mu4).  Readings (DESIGN.md c32-c35): u = z = 0, x_0 = 0, r~ = r_0 = b;
+# every compound update is evaluated left to right as a chain of single RN
+# operations (sub(a, b) = RN(a - b), scal(c, a) = RN(c a), axpy as above):
+#   beta = RN(RN(rho/rho_prev) * RN(alpha_prev/zeta))
+#   w = v + beta q;  p = r + beta (p - u);  s = t - r;  t = r - alpha q
+#   y = s - alpha (w - q)    (i = 1: y = RN(alpha q) - r)
+#   tau = RN(RN(mu5 mu1) - RN(mu4 mu4))
+#   zeta = RN(RN(RN(mu1 mu2) - RN(mu3 mu4)) / tau)
+#   eta  = RN(RN(RN(mu5 mu3) - RN(mu4 mu2)) / tau)
+#   (i = 1: zeta = mu2/mu5, or 0 when mu5 = 0 (then t = 0), eta = 0)
+#   u = RN(RN(zeta q) + RN(eta RN(s + RN(beta u))))   (i = 1: u = RN(zeta q))
+#   z = RN(RN(RN(zeta r) + RN(eta z)) - RN(alpha u))
+#   x = RN(RN(x + RN(alpha p)) + z)
+#   r = RN(RN(t - RN(eta y)) - RN(zeta v))
+# The figure prints "z = zeta r + zeta z - alpha u" and "r = t - eta y -
+# zeta u"; read literally the method does not converge (a diagonally dominant
+# band where BiCG converges in 39 iterations stalls for 200); these are read as
+# the typos of Zhang's GPBiCG (1997), which the paper implements: eta z and
+# zeta v (v = A t).
+# The figure's convergence check (*) sits before r_i is formed; it is applied
+# to r_i (the residual it tests).  Breakdown: rho = 0, (r~, q) = 0, tau = 0,
+# or zeta = 0 for an iteration that did not converge.
+# --------------------------------------------------------------------------
+
+def sub(a, b, p):
+    return [add(x, neg(y), p) for x, y in zip(a, b)]
+
+
+def scal(c, a, p):
+    return [mul(c, x, p) for x in a]
+
+
+def vadd(a, b, p):
+    return [add(x, y, p) for x, y in zip(a, b)]
+
+
+def gpbicg(p: int, A, b, max_iter: int, trace: bool = False):
+    n = len(b)
+    c1, c2 = recip_pow10(20, p), recip_pow10(50, p)
+    x = [ZERO] * n
+    r = list(b)
+    rt = list(r)
+    u = [ZERO] * n
+    z = [ZERO] * n
+    nrm0 = norm2(r, p)
+    thr = add(mul(c1, nrm0, p), c2, p)
+    norms = [nrm0]
+    hist = []
+    status, it = "max_iter", 0
+    rho_prev = alpha_prev = zeta = beta = None
+    pv = t = w = q = v = s = y = None
+    for i in range(1, max_iter + 1):
+        rho = dot(rt, r, p)
+        if rho[1] == 0:
+            status = "breakdown"
+            break
+        if i == 1:
+            pv = list(r)
+            q = _spmv_list(p, A, pv)
+            sq = dot(rt, q, p)
+            if sq[1] == 0:
+                status = "breakdown"
+                break
+            alpha = div(rho, sq, p)
+            t = axpy(alpha, q, r, p, negate=True)
+            v = _spmv_list(p, A, t)
+            y = sub(scal(alpha, q, p), r, p)
+            mu2, mu5 = dot(v, t, p), dot(v, v, p)
+            zeta = ZERO if mu5[1] == 0 else div(mu2, mu5, p)
+            eta = ZERO
+            u = scal(zeta, q, p)
+        else:
+            beta = mul(div(rho, rho_prev, p), div(alpha_prev, zeta, p), p)
+            w = axpy(beta, q, v, p)
+            pv = axpy(beta, sub(pv, u, p), r, p)
+            q = _spmv_list(p, A, pv)
+            sq = dot(rt, q, p)
+            if sq[1] == 0:
+                status = "breakdown"
+                break
+            alpha = div(rho, sq, p)
+            s = sub(t, r, p)
+            t = axpy(alpha, q, r, p, negate=True)
+            v = _spmv_list(p, A, t)
+            y = axpy(alpha, sub(w, q, p), s, p, negate=True)
+            mu1, mu2, mu3 = dot(y, y, p), dot(v, t, p), dot(y, t, p)
+            mu4, mu5 = dot(v, y, p), dot(v, v, p)
+            tau = add(mul(mu5, mu1, p), neg(mul(mu4, mu4, p)), p)
+            if tau[1] == 0:
+                status = "breakdown"
+                break
+            zeta = div(add(mul(mu1, mu2, p), neg(mul(mu3, mu4, p)), p), tau, p)
+            eta = div(add(mul(mu5, mu3, p), neg(mul(mu4, mu2, p)), p), tau, p)
+            u = axpy(eta, axpy(beta, u, s, p), scal(zeta, q, p), p)
+        z = axpy(alpha, u, vadd(scal(zeta, r, p), scal(eta, z, p), p), p, negate=True)
+        x = vadd(axpy(alpha, pv, x, p), z, p)
+        r = axpy(zeta, v, axpy(eta, y, t, p, negate=True), p, negate=True)
+        nrm = norm2(r, p)
+        norms.append(nrm)
+        it = i
+        if trace:
+            hist.append(dict(rho=rho, alpha=alpha, zeta=zeta, eta=eta, beta=beta, nrm=nrm))
+        rho_prev, alpha_prev = rho, alpha
+        if le(nrm, thr):
+            status = "converged"
+            break
+        if zeta[1] == 0:
+            status = "breakdown"
+            break
+    return dict(x=x, iters=it, status=status, norms=norms, thr=thr, hist=hist)

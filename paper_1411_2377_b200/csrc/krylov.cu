@@ -81,7 +81,10 @@ __global__ void __launch_bounds__(32) vec_dot(int64_t n, VecIn u, VecIn v, YView
 //     products.  Validation uses exactly the conditions WChain::consume
 //     checks block by block, so the result is the ordered chain's, bit for bit.
 // ---------------------------------------------------------------------------
-constexpr int DSEG_NB = 8;                       // blocks of 32 steps per segment
+#ifndef MPSP_DSEG_NB
+#define MPSP_DSEG_NB 4
+#endif
+constexpr int DSEG_NB = MPSP_DSEG_NB;            // blocks of 32 steps per segment
 constexpr int DSEG = 32 * DSEG_NB;
 
 struct DotWork {                                  // device scratch (sizes: dot_work_bytes)

@@ -167,3 +167,96 @@ def test_converges_on_diagonally_dominant_band(p):
     assert K.le(res["norms"][-1], res["thr"])
     for i, v in enumerate(res["x"]):
         assert abs(to_frac(v, p) - (i + 1)) < Fraction(1, 10 ** 15)
+
+
+def test_gpbicg_identity_converges_in_one_step():
+    p, n = 128, 10
+    rowptr = np.arange(n + 1, dtype=np.int64)
+    colidx = np.arange(n, dtype=np.int32)
+    limbs, exps, signs = oracle.pack_vec([K.from_int(1, p)] * n, p)
+    b = [K.from_int(i + 1, p) for i in range(n)]
+    res = K.gpbicg(p, (rowptr, colidx, limbs, exps, signs), b, 10)
+    assert res["status"] == "converged" and res["iters"] == 1
+    assert res["x"] == b
+
+
+@pytest.mark.parametrize("p", [128, 256])
+def test_gpbicg_converges_on_diagonally_dominant_band(p):
+    n = 40
+    A = _diag_dominant(n, p, 6)
+    rowptr, colidx, limbs, exps, signs = A
+    xt = [K.from_int(i + 1, p) for i in range(n)]
+    xl, xe, xs = oracle.pack_vec(xt, p)
+    b = oracle.unpack_vec(*oracle.spmv(p, rowptr, colidx, limbs, exps, signs, xl, xe, xs), p)
+    res = K.gpbicg(p, A, b, 200)
+    assert res["status"] == "converged", res["status"]
+    assert K.le(res["norms"][-1], res["thr"])
+    for i, v in enumerate(res["x"]):
+        assert abs(to_frac(v, p) - (i + 1)) < Fraction(1, 10 ** 15)
+    # same system, same solution as BiCG to the test's accuracy, and GPBiCG
+    # (transpose-free, two A products per iteration) does not need A^T
+    res_b = K.bicg(p, A, b, 200)
+    assert res_b["status"] == "converged"
+
+
+def _frac_gpbicg(Af, bf, iters):
+    """Zhang's GPBiCG in exact rational arithmetic (same readings)."""
+    n = len(bf)
+    mv = lambda v: [sum(Af[k][j] * v[j] for j in range(n)) for k in range(n)]
+    dp = lambda a, b: sum(x * y for x, y in zip(a, b))
+    x = [Fraction(0)] * n
+    r = list(bf)
+    rt = list(r)
+    u = [Fraction(0)] * n
+    z = [Fraction(0)] * n
+    out = []
+    for i in range(1, iters + 1):
+        rho = dp(rt, r)
+        if i == 1:
+            pv = list(r)
+            q = mv(pv)
+            alpha = rho / dp(rt, q)
+            t = [a - alpha * c for a, c in zip(r, q)]
+            v = mv(t)
+            y = [alpha * c - a for a, c in zip(r, q)]
+            zeta, eta = dp(v, t) / dp(v, v), Fraction(0)
+            u = [zeta * c for c in q]
+        else:
+            beta = (rho / rho_prev) * (alpha_prev / zeta)
+            w = [a + beta * c for a, c in zip(v, q)]
+            pv = [a + beta * (c - d) for a, c, d in zip(r, pv, u)]
+            q = mv(pv)
+            alpha = rho / dp(rt, q)
+            s = [a - c for a, c in zip(t, r)]
+            t = [a - alpha * c for a, c in zip(r, q)]
+            v = mv(t)
+            y = [a - alpha * (c - d) for a, c, d in zip(s, w, q)]
+            m1, m2, m3, m4, m5 = dp(y, y), dp(v, t), dp(y, t), dp(v, y), dp(v, v)
+            tau = m5 * m1 - m4 * m4
+            zeta = (m1 * m2 - m3 * m4) / tau
+            eta = (m5 * m3 - m4 * m2) / tau
+            u = [zeta * c + eta * (a + beta * d) for c, a, d in zip(q, s, u)]
+        z = [zeta * a + eta * c - alpha * d for a, c, d in zip(r, z, u)]
+        x = [a + alpha * c + d for a, c, d in zip(x, pv, z)]
+        r = [a - eta * c - zeta * d for a, c, d in zip(t, y, v)]
+        out.append(x)
+        rho_prev, alpha_prev = rho, alpha
+    return out
+
+
+def test_gpbicg_first_iterates_match_exact_rational():
+    p, n = 256, 8
+    A = _diag_dominant(n, p, 4)
+    rowptr, colidx, limbs, exps, signs = A
+    vals = oracle.unpack_vec(limbs, exps, signs, p)
+    Af = [[Fraction(0)] * n for _ in range(n)]
+    for i in range(n):
+        for k in range(rowptr[i], rowptr[i + 1]):
+            Af[i][colidx[k]] = to_frac(vals[k], p)
+    xl, xe, xs = oracle.pack_vec([K.from_int(i + 1, p) for i in range(n)], p)
+    b = oracle.unpack_vec(*oracle.spmv(p, rowptr, colidx, limbs, exps, signs, xl, xe, xs), p)
+    res = K.gpbicg(p, A, b, 3)
+    exact = _frac_gpbicg(Af, [to_frac(v, p) for v in b], res["iters"])
+    for i in range(n):
+        got, want = to_frac(res["x"][i], p), exact[-1][i]
+        assert abs(got - want) <= abs(want) * Fraction(1, 2 ** 230) + Fraction(1, 2 ** 240)
