@@ -201,6 +201,17 @@ int mpsp_bicg(mpsp_csr *A,
               uint32_t *x_limbs, int32_t *x_exps, uint8_t *x_signs,
               int max_iter, int *iters, int *status, void *cuda_stream);
 
+/* Solve A x = b by GPBiCG (Fig. 4 right; K = I; readings
+ * c32-c35 in DESIGN.md: left-to-right RN evaluation of every compound
+ * update, the figure's "zeta z" / "zeta u" read as eta z / zeta v).
+ * Transpose-free: A needs no MPSP_WITH_TRANSPOSE.  Same arguments, status
+ * and errors as mpsp_bicg (breakdown also on tau = 0 or zeta = 0).
+ * Workspace: 14 n-vectors, allocated and freed per call. */
+int mpsp_gpbicg(mpsp_csr *A,
+                const uint32_t *b_limbs, const int32_t *b_exps, const uint8_t *b_signs,
+                uint32_t *x_limbs, int32_t *x_exps, uint8_t *x_signs,
+                int max_iter, int *iters, int *status, void *cuda_stream);
+
 /* Diagnostics of the segmented dot: out[0] = segments the
  * chain warp evaluated step by step, out[1] = segments committed from their
  * speculative sums, since the last call (counters are then reset). */

@@ -24,7 +24,7 @@ ERROR_CODES = {v: k for k, v in ERRORS.items()}
 SYMBOLS = ("mpsp_csr_create", "mpsp_spmv", "mpsp_spmv_t", "mpsp_spmv_host", "mpsp_spmv_t_host",
            "mpsp_destroy", "mpsp_strerror", "mpsp_last_cuda_error", "mpsp_csr_info",
            "mpsp_launch_count", "mpsp_imad_bench", "mpsp_supported_precision",
-           "mpsp_dot", "mpsp_axpy", "mpsp_bicg", "mpsp_debug_dot_stats")
+           "mpsp_dot", "mpsp_axpy", "mpsp_bicg", "mpsp_gpbicg", "mpsp_debug_dot_stats")
 BICG_STATUS = {0: "converged", 1: "breakdown", 2: "max_iter"}
 
 
@@ -82,6 +82,8 @@ def lib() -> ctypes.CDLL:
     L.mpsp_axpy.restype = I
     L.mpsp_bicg.argtypes = [P, P, P, P, P, P, P, I, ctypes.POINTER(I), ctypes.POINTER(I), P]
     L.mpsp_bicg.restype = I
+    L.mpsp_gpbicg.argtypes = L.mpsp_bicg.argtypes
+    L.mpsp_gpbicg.restype = I
     L.mpsp_debug_dot_stats.argtypes = [P]
     L.mpsp_debug_dot_stats.restype = I
     _lib = L

@@ -139,20 +139,29 @@ class CSR:
     def spmv_t_host(self, xl, xe, xs, out=None):
         return self._host(_lib.lib().mpsp_spmv_t_host, xl, xe, xs, out)
 
+    def gpbicg(self, b: MPVec, max_iter: int, x: MPVec | None = None, stream=None):
+        """Solve A x = b by GPBiCG (Fig. 4 right, K = I; mpsp_gpbicg).
+        Transpose-free; full-matrix handle, p >= 128.  Returns (x, iterations,
+        status)."""
+        return self._solve(_lib.lib().mpsp_gpbicg, b, max_iter, x, stream)
+
     def bicg(self, b: MPVec, max_iter: int, x: MPVec | None = None, stream=None):
         """Solve A x = b by BiCG (Fig. 4, K = I; mpsp_bicg).  Needs a
         full-matrix handle built with transpose=True and p >= 128.  Returns
         (x, iterations, status) with status "converged" | "breakdown" |
         "max_iter"."""
+        return self._solve(_lib.lib().mpsp_bicg, b, max_iter, x, stream)
+
+    def _solve(self, fn, b, max_iter, x, stream):
         if x is None:
             x = MPVec.empty(self.n, self.L, device=b.limbs.device)
         if stream is None:
             stream = torch.cuda.current_stream(b.limbs.device).cuda_stream
         it, st = ctypes.c_int(0), ctypes.c_int(0)
-        rc = _lib.lib().mpsp_bicg(self._h, _ptr(b.limbs), _ptr(b.exps), _ptr(b.signs),
-                                  _ptr(x.limbs), _ptr(x.exps), _ptr(x.signs), int(max_iter),
-                                  ctypes.byref(it), ctypes.byref(st), ctypes.c_void_p(stream))
-        _lib.check(rc, "mpsp_bicg")
+        rc = fn(self._h, _ptr(b.limbs), _ptr(b.exps), _ptr(b.signs), _ptr(x.limbs),
+                _ptr(x.exps), _ptr(x.signs), int(max_iter), ctypes.byref(it), ctypes.byref(st),
+                ctypes.c_void_p(stream))
+        _lib.check(rc, fn.__name__)
         return x, it.value, _lib.BICG_STATUS[st.value]
 
     def close(self):

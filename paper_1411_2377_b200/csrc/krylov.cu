@@ -413,8 +413,25 @@ __device__ int mp_cmp(const MP<L>& a, const MP<L>& b) {
 // BiCG scalars (device, ABI format [NSC] elements) and flags
 enum { S_RHO = KS_RHO, S_RHOP = KS_RHOP, S_SIGMA = KS_SIGMA, S_ALPHA = KS_ALPHA, S_BETA = KS_BETA,
        S_RR = KS_RR, S_NRM = KS_NRM, S_THR = KS_THR, S_C1 = KS_C1, S_C2 = KS_C2, S_ONE = KS_ONE,
-       S_T20 = KS_T20, S_T50 = KS_T50 };
-enum { F_STOP = KF_STOP, F_BREAK = KF_BREAK, F_CONV = KF_CONV };
+       S_T20 = KS_T20, S_T50 = KS_T50, S_ALPHAP = KS_ALPHAP, S_ZETA = KS_ZETA, S_ETA = KS_ETA,
+       S_MU1 = KS_MU1, S_MU2 = KS_MU2, S_MU3 = KS_MU3, S_MU4 = KS_MU4, S_MU5 = KS_MU5,
+       S_TAU = KS_TAU };
+enum { F_STOP = KF_STOP, F_BREAK = KF_BREAK, F_CONV = KF_CONV, F_BRK2 = KF_BRK2 };
+
+template <int L>
+__device__ __forceinline__ void sc_mul(const MP<L>& a, const MP<L>& b, MP<L>& o) {
+  mp_mul<L>(a.m, a.e, a.s, b.m, b.e, b.s, o);
+}
+// o = RN(RN(a b) - RN(c d))
+template <int L>
+__device__ __forceinline__ void sc_det(const MP<L>& a, const MP<L>& b, const MP<L>& c,
+                                       const MP<L>& d, MP<L>& o) {
+  MP<L> t;
+  sc_mul<L>(a, b, o);
+  sc_mul<L>(c, d, t);
+  t.s ^= 1u;
+  mp_add<L>(o, t);
+}
 
 template <int L>
 __device__ __forceinline__ void sc_load(const YView& S, int i, MP<L>& a) {
@@ -427,6 +444,13 @@ __device__ __forceinline__ void sc_load(const YView& S, int i, MP<L>& a) {
 //     1 rho check (rho == 0 -> breakdown)    2 beta = rho / rho_prev
 //     3 alpha = rho / sigma (sigma == 0 -> breakdown)
 //     4 nrm = sqrt(rr), converged iff nrm <= thr; rho_prev = rho
+//   GPBiCG (readings c32-c35 of DESIGN.md):
+//     5 zeta = mu5 == 0 ? 0 : mu2 / mu5, eta = 0              (first iteration)
+//     6 beta = RN(RN(rho / rho_prev) * RN(alpha_prev / zeta))
+//     7 tau = RN(RN(mu5 mu1) - RN(mu4 mu4)) (0 -> breakdown),
+//       zeta = RN(RN(RN(mu1 mu2) - RN(mu3 mu4)) / tau), eta = RN(RN(RN(mu5 mu3) - RN(mu4 mu2)) / tau)
+//     8 nrm = sqrt(rr), converged iff nrm <= thr, else zeta = 0 -> breakdown;
+//       rho_prev = rho, alpha_prev = alpha
 template <int L>
 __global__ void bicg_scalar(YView S, int* fl, int op) {
   if (fl[F_STOP]) return;
@@ -476,6 +500,62 @@ __global__ void bicg_scalar(YView S, int* fl, int op) {
       if (mp_cmp<L>(b, c) <= 0) { fl[F_CONV] = 1; fl[F_STOP] = 1; }
       sc_load<L>(S, S_RHO, a);
       store_y<L>(S, S_RHOP, a);
+      break;
+    }
+    case 5: {
+      sc_load<L>(S, S_MU2, a);
+      sc_load<L>(S, S_MU5, b);
+      if (b.is_zero()) c.set_zero(); else mp_div<L>(a, b, c);
+      store_y<L>(S, S_ZETA, c);
+      c.set_zero();
+      store_y<L>(S, S_ETA, c);
+      break;
+    }
+    case 6: {
+      MP<L> d, e;
+      sc_load<L>(S, S_RHO, a);
+      sc_load<L>(S, S_RHOP, b);
+      mp_div<L>(a, b, c);
+      sc_load<L>(S, S_ALPHAP, a);
+      sc_load<L>(S, S_ZETA, b);
+      mp_div<L>(a, b, d);
+      sc_mul<L>(c, d, e);
+      store_y<L>(S, S_BETA, e);
+      break;
+    }
+    case 7: {
+      MP<L> m1, m2, m3, m4, m5, tau, num;
+      sc_load<L>(S, S_MU1, m1);
+      sc_load<L>(S, S_MU2, m2);
+      sc_load<L>(S, S_MU3, m3);
+      sc_load<L>(S, S_MU4, m4);
+      sc_load<L>(S, S_MU5, m5);
+      sc_det<L>(m5, m1, m4, m4, tau);
+      store_y<L>(S, S_TAU, tau);
+      if (tau.is_zero()) { fl[F_BREAK] = 1; fl[F_STOP] = 1; break; }
+      sc_det<L>(m1, m2, m3, m4, num);
+      mp_div<L>(num, tau, c);
+      store_y<L>(S, S_ZETA, c);
+      sc_det<L>(m5, m3, m4, m2, num);
+      mp_div<L>(num, tau, c);
+      store_y<L>(S, S_ETA, c);
+      break;
+    }
+    case 8: {
+      sc_load<L>(S, S_RR, a);
+      mp_sqrt<L>(a, b);
+      store_y<L>(S, S_NRM, b);
+      sc_load<L>(S, S_THR, c);
+      if (mp_cmp<L>(b, c) <= 0) {
+        fl[F_CONV] = 1; fl[F_STOP] = 1;
+      } else {
+        sc_load<L>(S, S_ZETA, a);
+        if (a.is_zero()) { fl[F_BRK2] = 1; fl[F_STOP] = 1; }
+      }
+      sc_load<L>(S, S_RHO, a);
+      store_y<L>(S, S_RHOP, a);
+      sc_load<L>(S, S_ALPHA, a);
+      store_y<L>(S, S_ALPHAP, a);
       break;
     }
   }

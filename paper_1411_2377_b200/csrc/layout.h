@@ -92,8 +92,10 @@ int krylov_axpy(int L, int64_t n, const VecIn& al, int neg, const VecIn& x, cons
                 const YView& z, const int* stop, void* stream);
 int krylov_scalar(int L, const YView& S, int* fl, int op, void* stream);
 enum { KS_RHO, KS_RHOP, KS_SIGMA, KS_ALPHA, KS_BETA, KS_RR, KS_NRM, KS_THR, KS_C1, KS_C2, KS_ONE,
-       KS_T20, KS_T50, KS_N };
-enum { KF_STOP, KF_BREAK, KF_CONV, KF_N };
+       KS_T20, KS_T50, KS_ALPHAP, KS_ZETA, KS_ETA, KS_MU1, KS_MU2, KS_MU3, KS_MU4, KS_MU5, KS_TAU,
+       KS_N };
+// KF_BRK2: breakdown detected after the iteration's update (GPBiCG zeta = 0)
+enum { KF_STOP, KF_BREAK, KF_CONV, KF_BRK2, KF_N };
 // Integer-MAC microbenchmark (roofline denominator); returns cudaError_t.
 int run_imad_bench(double out[3]);
 // Launches this process has made.

@@ -750,7 +750,7 @@ int mpsp_bicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, const
   cp(bv, rt);
   K(krylov_dot(L, n, in(r), in(r), sc_out(KS_RR), fl, st, dwork));
   K(krylov_scalar(L, S, fl, 0, st));
-  int hfl[KF_N] = {0, 0, 0};
+  int hfl[KF_N] = {0, 0, 0, 0};
   for (int i = 1; i <= max_iter && rc == MPSP_OK; ++i) {
     K(krylov_dot(L, n, in(rt), in(r), sc_out(KS_RHO), fl, st, dwork));
     K(krylov_scalar(L, S, fl, 1, st));                       // rho == 0 -> stop
@@ -781,6 +781,155 @@ int mpsp_bicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, const
     if (hfl[KF_BREAK]) { *status = MPSP_BICG_BREAKDOWN; break; }
     *iters = i;
     if (hfl[KF_CONV]) { *status = MPSP_BICG_CONVERGED; break; }
+  }
+  cudaStreamSynchronize(st);
+  cudaFree(ws);
+  return rc;
+}
+
+int mpsp_gpbicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, const uint8_t* b_signs,
+                uint32_t* x_limbs, int32_t* x_exps, uint8_t* x_signs, int max_iter, int* iters,
+                int* status, void* cuda_stream) {
+  if (!A || !iters || !status || max_iter < 0) return MPSP_E_ARG;
+  if (A->rb != 0 || A->re != A->n) return MPSP_E_ARG;   // needs the whole matrix
+  if (A->p < 128) return MPSP_E_PREC;
+  const int L = A->L;
+  const int64_t n = A->n;
+  *iters = 0;
+  *status = MPSP_BICG_MAXITER;
+  if (n > 0 && (!b_limbs || !b_exps || !b_signs || !x_limbs || !x_exps || !x_signs)) return MPSP_E_ARG;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  cudaError_t ce;
+  constexpr int NV = 12;        // r rt u z p q t v w s y zero, + 2 temporaries
+  const size_t vl = (size_t)n * L * 4, ve = (size_t)n * 4, vs = (size_t)n;
+  auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  const size_t per = al(vl) + al(ve) + al(vs);
+  const size_t sbytes = al((size_t)KS_N * L * 4) + al((size_t)KS_N * 4) + al(KS_N) + 256;
+  const size_t dbytes = al(krylov_dot_work_bytes(L, n));
+  char* ws = nullptr;
+  if ((ce = cudaMalloc(&ws, (NV + 2) * per + sbytes + dbytes)) != cudaSuccess) {
+    cudaGetLastError();
+    return MPSP_E_NOMEM;
+  }
+  void* dwork = dbytes ? (void*)(ws + (NV + 2) * per + sbytes) : nullptr;
+  struct V { uint32_t* l; int32_t* e; uint8_t* s; };
+  V vec[NV + 2];
+  for (int i = 0; i < NV + 2; ++i) {
+    char* b0 = ws + i * per;
+    vec[i] = V{(uint32_t*)b0, (int32_t*)(b0 + al(vl)), (uint8_t*)(b0 + al(vl) + al(ve))};
+  }
+  char* sb = ws + (NV + 2) * per;
+  YView S{(uint32_t*)sb, (int32_t*)(sb + al((size_t)KS_N * L * 4)),
+          (uint8_t*)(sb + al((size_t)KS_N * L * 4) + al((size_t)KS_N * 4))};
+  int* fl = (int*)(sb + al((size_t)KS_N * L * 4) + al((size_t)KS_N * 4) + al(KS_N));
+  V &r = vec[0], &rt = vec[1], &u = vec[2], &z = vec[3], &pv = vec[4], &q = vec[5], &t = vec[6],
+    &v = vec[7], &w = vec[8], &sv = vec[9], &y = vec[10], &zero = vec[11], &t1 = vec[12], &t2 = vec[13];
+  V xv{x_limbs, x_exps, x_signs};
+  V bv{(uint32_t*)b_limbs, (int32_t*)b_exps, (uint8_t*)b_signs};
+  auto in = [](const V& a) { return VecIn{a.l, a.e, a.s}; };
+  auto out = [](const V& a) { return YView{a.l, a.e, a.s}; };
+  auto sc_in = [&](int i) { return VecIn{S.limbs + (size_t)i * L, S.exps + i, S.signs + i}; };
+  auto sc_out = [&](int i) { return YView{S.limbs + (size_t)i * L, S.exps + i, S.signs + i}; };
+  int rc = MPSP_OK;
+  auto K = [&](int e) { if (e && rc == MPSP_OK) rc = cuda_fail((cudaError_t)e); };
+  auto zero_v = [&](const V& a) {
+    if (n == 0) return;
+    K((int)cudaMemsetAsync(a.l, 0, vl, st));
+    K((int)cudaMemsetAsync(a.e, 0, ve, st));
+    K((int)cudaMemsetAsync(a.s, 0, vs, st));
+  };
+  auto cp = [&](const V& src, const V& dst) {
+    if (n == 0) return;
+    K((int)cudaMemcpyAsync(dst.l, src.l, vl, cudaMemcpyDeviceToDevice, st));
+    K((int)cudaMemcpyAsync(dst.e, src.e, ve, cudaMemcpyDeviceToDevice, st));
+    K((int)cudaMemcpyAsync(dst.s, src.s, vs, cudaMemcpyDeviceToDevice, st));
+  };
+  // out = RN(y + RN(+-c x)): the one vector kernel every update is built from
+  auto ax = [&](int c, bool neg, const V& xx, const V& yy, const V& oo) {
+    K(krylov_axpy(L, n, sc_in(c), neg ? 1 : 0, in(xx), in(yy), out(oo), fl, st));
+  };
+  auto spmv = [&](const V& src, const V& dst) {
+    const int e = do_spmv(A, false, src.l, src.e, src.s, dst.l, dst.e, dst.s, cuda_stream, false);
+    if (e != MPSP_OK && rc == MPSP_OK) rc = e;
+  };
+  auto dotv = [&](const V& a, const V& b2, int slot) {
+    K(krylov_dot(L, n, in(a), in(b2), sc_out(slot), fl, st, dwork));
+  };
+  auto scal = [&](int op) { K(krylov_scalar(L, S, fl, op, st)); };
+  {
+    std::vector<uint32_t> hl((size_t)KS_N * L, 0u);
+    std::vector<int32_t> he(KS_N, 0);
+    std::vector<uint8_t> hs(KS_N, 0);
+    encode_int(L, &hl[(size_t)KS_ONE * L], &he[KS_ONE], &hs[KS_ONE], {1u});
+    encode_int(L, &hl[(size_t)KS_T20 * L], &he[KS_T20], &hs[KS_T20], pow10_words(20));
+    encode_int(L, &hl[(size_t)KS_T50 * L], &he[KS_T50], &hs[KS_T50], pow10_words(50));
+    K((int)cudaMemcpyAsync(S.limbs, hl.data(), hl.size() * 4, cudaMemcpyHostToDevice, st));
+    K((int)cudaMemcpyAsync(S.exps, he.data(), he.size() * 4, cudaMemcpyHostToDevice, st));
+    K((int)cudaMemcpyAsync(S.signs, hs.data(), hs.size(), cudaMemcpyHostToDevice, st));
+    K((int)cudaMemsetAsync(fl, 0, KF_N * sizeof(int), st));
+    K((int)cudaStreamSynchronize(st));
+  }
+  zero_v(xv); zero_v(u); zero_v(z); zero_v(zero);
+  cp(bv, r);
+  cp(bv, rt);
+  dotv(r, r, KS_RR);
+  scal(0);                                                    // c1, c2, thr
+  int hfl[KF_N] = {0, 0, 0, 0};
+  for (int i = 1; i <= max_iter && rc == MPSP_OK; ++i) {
+    dotv(rt, r, KS_RHO);
+    scal(1);                                                  // rho == 0
+    if (i == 1) {
+      cp(r, pv);
+      spmv(pv, q);
+      dotv(rt, q, KS_SIGMA);
+      scal(3);                                                // alpha = rho / (r~, q)
+      ax(KS_ALPHA, true, q, r, t);                            // t = r - alpha q
+      spmv(t, v);
+      ax(KS_ALPHA, false, q, zero, t1);                       // y = alpha q - r
+      ax(KS_ONE, true, r, t1, y);
+      dotv(v, t, KS_MU2);
+      dotv(v, v, KS_MU5);
+      scal(5);                                                // zeta, eta = 0
+      ax(KS_ZETA, false, q, zero, u);                         // u = zeta q
+    } else {
+      scal(6);                                                // beta
+      ax(KS_BETA, false, q, v, w);                            // w = v + beta q
+      ax(KS_ONE, true, u, pv, t1);                            // p = r + beta (p - u)
+      ax(KS_BETA, false, t1, r, pv);
+      spmv(pv, q);
+      dotv(rt, q, KS_SIGMA);
+      scal(3);                                                // alpha
+      ax(KS_ONE, true, r, t, sv);                             // s = t - r
+      ax(KS_ALPHA, true, q, r, t);                            // t = r - alpha q
+      spmv(t, v);
+      ax(KS_ONE, true, q, w, t1);                             // y = s - alpha (w - q)
+      ax(KS_ALPHA, true, t1, sv, y);
+      dotv(y, y, KS_MU1);
+      dotv(v, t, KS_MU2);
+      dotv(y, t, KS_MU3);
+      dotv(v, y, KS_MU4);
+      dotv(v, v, KS_MU5);
+      scal(7);                                                // tau, zeta, eta
+      ax(KS_BETA, false, u, sv, t1);                          // u = zeta q + eta (s + beta u)
+      ax(KS_ZETA, false, q, zero, t2);
+      ax(KS_ETA, false, t1, t2, u);
+    }
+    ax(KS_ZETA, false, r, zero, t1);                          // z = zeta r + eta z - alpha u
+    ax(KS_ETA, false, z, t1, t1);
+    ax(KS_ALPHA, true, u, t1, z);
+    ax(KS_ALPHA, false, pv, xv, t1);                          // x = x + alpha p + z
+    ax(KS_ONE, false, z, t1, xv);
+    ax(KS_ETA, true, y, t, t1);                               // r = t - eta y - zeta v
+    ax(KS_ZETA, true, v, t1, r);
+    dotv(r, r, KS_RR);
+    scal(8);                                                  // converged / zeta == 0
+    K((int)cudaMemcpyAsync(hfl, fl, sizeof hfl, cudaMemcpyDeviceToHost, st));
+    K((int)cudaStreamSynchronize(st));
+    if (rc != MPSP_OK) break;
+    if (hfl[KF_BREAK]) { *status = MPSP_BICG_BREAKDOWN; break; }
+    *iters = i;
+    if (hfl[KF_CONV]) { *status = MPSP_BICG_CONVERGED; break; }
+    if (hfl[KF_BRK2]) { *status = MPSP_BICG_BREAKDOWN; break; }
   }
   cudaStreamSynchronize(st);
   cudaFree(ws);

@@ -200,3 +200,35 @@ def test_dot_segmented_paths(kind, p, n):
         assert st["validated"] == 0              # overflowing guesses never commit
     if kind == "positive":
         assert st["validated"] > st["sequential"]   # the speculative path carries the chain
+
+
+@pytest.mark.parametrize("kind,n,p,max_iter", [("band", 60, 128, 200), ("band", 150, 256, 300),
+                                               ("random", 80, 128, 300), ("band", 40, 512, 100),
+                                               ("band", 30, 1024, 4), ("random", 50, 256, 6)])
+def test_gpbicg_parity(kind, n, p, max_iter):
+    import torch
+    from paper_1411_2377_b200 import CSR
+    A, b = _system(kind, n, p, seed=3 * n + p)
+    want = K.gpbicg(p, A, b, max_iter)
+    H = CSR(p, *A)                                 # transpose-free: no A^T needed
+    x, it, status = H.gpbicg(_vec(b, p), max_iter)
+    torch.cuda.synchronize()
+    assert (it, status) == (want["iters"], want["status"])
+    assert_same(x.to_host(), oracle.pack_vec(want["x"], p), f"gpbicg {kind} n={n} p={p}")
+    H.close()
+
+
+def test_gpbicg_identity():
+    import torch
+    from paper_1411_2377_b200 import CSR
+    p, n = 256, 33
+    limbs, exps, signs = oracle.pack_vec([K.from_int(1, p)] * n, p)
+    rowptr = np.arange(n + 1, dtype=np.int64)
+    colidx = np.arange(n, dtype=np.int32)
+    b = [K.from_int(i + 1, p) for i in range(n)]
+    H = CSR(p, rowptr, colidx, limbs, exps, signs)
+    x, it, status = H.gpbicg(_vec(b, p), 10)
+    torch.cuda.synchronize()
+    assert (it, status) == (1, "converged")
+    assert_same(x.to_host(), oracle.pack_vec(b, p), "gpbicg identity")
+    H.close()
