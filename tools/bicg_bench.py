@@ -68,6 +68,13 @@ from paper_1411_2377_b200 import _lib  # noqa: E402
 st = (ctypes.c_ulonglong * 2)()
 _lib.lib().mpsp_debug_dot_stats(st)
 print("dot segments over the run: sequential", st[0], "validated", st[1])
+e0.record()
+xg, itg, statusg = A.gpbicg(b, iters)
+e1.record()
+torch.cuda.synchronize()
+t_gp = e0.elapsed_time(e1)
+print(json.dumps({"workload": f"GPBiCG band+-5 n={n} p={p}", "iters": itg, "status": statusg,
+                  "ms_total": t_gp, "ms_per_iter": t_gp / max(itg, 1)}))
 print(json.dumps({"workload": f"BiCG band+-5 n={n} p={p}", "iters": it, "status": status,
                   "ms_total": t_total, "ms_per_iter": t_total / max(it, 1),
                   "ms_dot": t_dot, "ms_spmv": t_spmv, "ms_spmv_t": t_spmvt, "ms_axpy": t_axpy,
