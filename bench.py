@@ -348,7 +348,7 @@ def main():
             roof["traffic"] = rec["traffic_bytes"]
             roof["traffic_source"] = f"profiles/{rec['summary'] or rec['report']} ({rec['kernel']})"
             roof["algorithmic_bytes"] = bytes_local
-    thr = int(os.environ.get("MPSP_LONG_T", "128"))
+    thr = int(os.environ.get("MPSP_LONG_T", "192"))
     sell = f"spmv_sell_cp<{L}>" if L == 32 and os.environ.get("MPSP_CP", "1") != "0" else f"spmv_sell<{L}>"
     roof["kernel"] = (sell if d["meta"]["max_row"] <= thr or args.op == "atx" else
                       f"{sell} + spmv_wrow<{L}> (concurrent streams, fork/join timed as one)")

@@ -39,7 +39,7 @@ namespace mpsp {
 // (tests lower it to route rows of any length through this kernel).
 int long_row_threshold() {
   const char* v = std::getenv("MPSP_LONG_T");
-  return v ? std::atoi(v) : 128;
+  return v ? std::atoi(v) : 192;
 }
 
 // Rows at least this long (and above the warp-row threshold) go to the
