@@ -206,11 +206,9 @@ __global__ void __launch_bounds__(128) dot_speculate(DotWork W, int64_t nseg, co
     W.maxv[seg] = mx;
     W.htot[seg] = base;
   }
-  if (lane < N) {
-    uint32_t v = R[0];
+  if (lane == 0) {                                 // all N limbs (N = L+2 may exceed 32)
 #pragma unroll
-    for (int i = 1; i < N; ++i) v = (lane == i) ? R[i] : v;
-    W.ds[seg * N + lane] = v;
+    for (int i = 0; i < N; ++i) W.ds[seg * N + i] = R[i];
   }
 }
 

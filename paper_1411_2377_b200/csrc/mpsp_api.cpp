@@ -655,7 +655,8 @@ int mpsp_dot(int p_bits, int64_t n, const uint32_t* u_limbs, const int32_t* u_ex
   // segmented parallel evaluation needs a scratch buffer (stream-ordered)
   cudaStream_t st = (cudaStream_t)cuda_stream;
   void* work = nullptr;
-  const size_t wb = krylov_dot_work_bytes(L, n);
+  const char* ns = std::getenv("MPSP_DOT_ONEWARP");           // debug: plain one-warp chain
+  const size_t wb = (ns && ns[0] == '1') ? 0 : krylov_dot_work_bytes(L, n);
   if (wb && cudaMallocAsync(&work, wb, st) != cudaSuccess) { cudaGetLastError(); return MPSP_E_NOMEM; }
   const int e = krylov_dot(L, n, u, v, o, nullptr, cuda_stream, work);
   if (work) cudaFreeAsync(work, st);

@@ -191,9 +191,90 @@ struct WChain {
         err = min(err + 32, 1 << 28);                 // saturates: checks then fail
         break;
       }
-      // ---- exact path at the first failing step f
+      // ---- the first failing step f
       const int f = __ffs(failM) - 1;
       if (lane < f) add_n<N>(R, R, Q);               // steps before f are valid
+      // One-binade transitions (tests/test_kernel_algorithms.py models them):
+      // if step f's exact sum V = S + tau provably crosses 2^p (equal signs)
+      // or provably lands in [2^(p-2), 2^(p-1)) (opposite signs), it is
+      // rounded directly on the new grid 2u / u/2 from the low bits of
+      // W = S (+ floor tau) - read off the lanes' R by ballots - and tau's
+      // fraction bits; R is halved / doubled lane by lane.  Everything else
+      // takes the exact path below.
+      {
+        const uint32_t fy = Y[0];                     // tau's 32 fraction bits
+        const bool fnz = (fy != 0u) || (stk != 0u);   // fraction != 0
+        const bool up_f = use && t.s == sg && LB + h - 1 >= HI;
+        const bool dn_f = use && t.s != sg && LB + ek + h + 2 <= LO && LB + h - 1 >= LO / 2;
+#ifdef MPSP_TRANS_MASK
+        const int mode = __shfl_sync(FULL, up_f ? 1 : (dn_f ? 2 : 0), f) & MPSP_TRANS_MASK;
+#else
+        const int mode = __shfl_sync(FULL, up_f ? 1 : (dn_f ? 2 : 0), f);
+#endif
+        if (mode != 0) {
+          const int32_t LBf = __shfl_sync(FULL, LB, f);
+          const int32_t hf = __shfl_sync(FULL, h, f);
+          const int32_t ekf = __shfl_sync(FULL, ek, f);
+          if (mode == 1) {                            // V in [2^p, 1.5 2^p): grid 2u
+            if (lane == f) {
+              uint32_t Yv[N];
+#pragma unroll
+              for (int i = 0; i < L; ++i) Yv[i] = Y[i + 1];
+              Yv[L] = 0u;
+              Yv[L + 1] = 0u;
+              add_n<N>(R, R, Yv);                     // W = S + floor(tau)
+            }
+            const uint32_t c0 = (uint32_t)__popc(__ballot_sync(FULL, R[0] & 1u));
+            const uint32_t c1 = (uint32_t)__popc(__ballot_sync(FULL, (R[0] >> 1) & 1u));
+            const uint32_t w0 = c0 & 1u, w1 = ((c0 >> 1) + c1) & 1u;
+            const uint32_t frac = __shfl_sync(FULL, fnz ? 1u : 0u, f);
+            const uint32_t incr = w0 & (frac | w1);   // RNE of W/2 + (w0 + frac)/2
+#pragma unroll
+            for (int i = 0; i < N - 1; ++i) R[i] = __funnelshift_r(R[i], R[i + 1], 1);
+            R[N - 1] = (uint32_t)((int32_t)R[N - 1] >> 1);
+            if (lane == 0) {
+              uint32_t Cv[N];
+              Cv[0] = (c0 >> 1) + incr;
+#pragma unroll
+              for (int i = 1; i < N; ++i) Cv[i] = 0u;
+              add_n<N>(R, R, Cv);                     // sum of halves + lost carries
+            }
+            E += 1;
+            Shi = (LBf + hf - 1) >> 1;
+            err = ((ekf + 3) >> 1) + 2;
+          } else {                                    // V in [2^(p-2), 2^(p-1)): grid u/2
+#pragma unroll
+            for (int i = N - 1; i > 0; --i) R[i] = __funnelshift_l(R[i - 1], R[i], 1);
+            R[0] <<= 1;
+            const uint32_t b1 = fy >> 31, b2 = (fy >> 30) & 1u;
+            const bool low = ((fy << 1) != 0u) || (stk != 0u);
+            const bool tie2 = b2 && ((fy << 2) == 0u) && (stk == 0u);
+            if (lane == f) {                          // R -= 2 floor(tau) + b1 (+1 if low)
+              uint32_t Yv[N];                         // (floor(tau) << 1) | b1
+#pragma unroll
+              for (int i = 0; i < N; ++i) {
+                const uint32_t lo_ = (i >= 1 && i - 1 < L) ? Y[i] : 0u;      // limb i-1
+                const uint32_t cur = (i < L) ? Y[i + 1] : 0u;                // limb i
+                Yv[i] = __funnelshift_l(lo_, cur, 1);
+              }
+              Yv[0] |= b1;
+              sub_n<N>(R, R, Yv, low ? 1u : 0u);
+            }
+            const uint32_t low_f = __shfl_sync(FULL, low ? 1u : 0u, f);
+            const uint32_t b1f = __shfl_sync(FULL, b1, f), b2f = __shfl_sync(FULL, b2, f);
+            const uint32_t tie2f = __shfl_sync(FULL, tie2 ? 1u : 0u, f);
+            if (lane == 0 && low_f) {
+              const uint32_t upb = (b2f == 0u) | (tie2f & (b1f ^ 1u));
+              inc_n<N>(R, upb);
+            }
+            E -= 1;
+            Shi = 2 * (LBf + hf - 1) - 2;
+            err = 2 * (ekf + 2) + 4;
+          }
+          start = f + 1;
+          continue;
+        }
+      }
       MP<L> s, tf;
       exact(s);
 #pragma unroll

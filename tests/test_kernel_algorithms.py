@@ -107,11 +107,15 @@ def test_short_product_tie_is_never_certified():
 HB = 26
 
 
-def block_sum_chain(ts, p, G=32, ties_exact=False):
+def block_sum_chain(ts, p, G=32, ties_exact=False, transitions=False, stats=None):
     """Model of spmv_wrow's chain over the products ts (oracle triples),
     G steps per block.  ties_exact=True models spmv_pcrow's chain warp, which
     sends a grid tie through the exact path instead of resolving its parity.
-    Returns (result, n_fast_steps)."""
+    transitions=True models WChain's one-binade transitions: a failing step
+    whose exact sum provably crosses 2^p (same signs) or provably drops to
+    [2^(p-2), 2^(p-1)) (opposite signs) is rounded on the new grid directly
+    (2u or u/2) from W's low bits and the step's fraction bits, without the
+    exact adder.  Returns (result, n_fast_steps)."""
     L = p // 32
     S, E, sg, zero = 0, 0, 0, True         # exact S (grid integer), exponent, sign
     Shi, err, par = 0, 0, 0
@@ -191,6 +195,49 @@ def block_sum_chain(ts, p, G=32, ties_exact=False):
             S += sum(Q[start:fail])
             nfast += cnt
             assert (1 << (p - 1)) <= S < (1 << p)
+            if transitions and not bad[fail]:
+                LBf = Shi + sum(hi(q) for q in Q[start:fail])
+                hf = hi(Q[fail])
+                ek = err + fail
+                st, Mt, Et = blk[fail]
+                d = min(E - Et, 32 * L + 32)
+                Y, rem = Mt >> d, Mt & ((1 << d) - 1)
+                LO, HI = 1 << (HB - 1), 1 << HB
+                if st == sg and LBf + hf - M1 >= HI:             # up: grid 2u
+                    W = S + Y
+                    inc = (W & 1) & (1 if (rem != 0 or (W >> 1) & 1) else 0)
+                    S = (W >> 1) + inc
+                    E += 1
+                    Shi, err = (LBf + hf - 1) >> 1, ((ek + 3) >> 1) + 2
+                    par = S & 1                                  # (the kernel reads it off R)
+                    assert (1 << (p - 1)) <= S < (1 << p)
+                    assert Shi <= hi(S) and hi(S) < Shi + err
+                    if stats is not None:
+                        stats["up"] = stats.get("up", 0) + 1
+                    start = fail + 1
+                    continue
+                if st != sg and LBf + ek + hf + 2 <= LO and LBf + hf - M1 >= LO // 2:   # down: u/2
+                    b1 = (rem >> (d - 1)) & 1
+                    b2 = (rem >> (d - 2)) & 1 if d >= 2 else 0
+                    low = rem & ((1 << (d - 1)) - 1)
+                    I = 2 * S - (2 * Y + b1)
+                    if low == 0:
+                        S = I
+                    else:
+                        tie2 = b2 == 1 and (low & ((1 << max(d - 2, 0)) - 1)) == 0
+                        up = (b2 == 0) or (tie2 and b1 == 0)
+                        S = I - 1 + (1 if up else 0)
+                    E -= 1
+                    Shi, err = 2 * (LBf + hf - M1) - 2, 2 * (ek + 2) + 4
+                    par = S & 1
+                    assert (1 << (p - 1)) <= S < (1 << p)
+                    assert Shi <= hi(S) and hi(S) < Shi + err
+                    if stats is not None:
+                        stats["down"] = stats.get("down", 0) + 1
+                    start = fail + 1
+                    continue
+            if stats is not None:
+                stats["exact"] = stats.get("exact", 0) + 1
             r = oracle.add((sg, S, E), blk[fail], p)
             sg, S, E = r
             zero = S == 0
@@ -253,3 +300,43 @@ def test_block_sum_ties_cancellation_and_zeros(p):
         assert got == oracle_chain(ts, p), trial
         got, _ = block_sum_chain(ts, p, G=rng.choice([64, 128]), ties_exact=True)
         assert got == oracle_chain(ts, p), ("ties exact", trial)
+
+
+@pytest.mark.parametrize("p", [32, 64, 128, 256])
+def test_block_sum_one_binade_transitions(p):
+    """Random walks (random signs, similar magnitudes) cross binade boundaries
+    all the time: most crossings must be taken by the one-binade transitions,
+    and every result must still be the ordered chain's."""
+    rng = random.Random(11 * p)
+    st = {}
+    for trial in range(30):
+        n = rng.choice([200, 600, 1500])
+        ts = [_rand_t(rng, p, -3, 3) for _ in range(n)]
+        got, _ = block_sum_chain(ts, p, transitions=True, stats=st)
+        assert got == oracle_chain(ts, p), trial
+        got, _ = block_sum_chain(ts, p, G=rng.choice([4, 32]), transitions=True, ties_exact=True,
+                                 stats=st)
+        assert got == oracle_chain(ts, p), ("ties exact", trial)
+    assert st.get("up", 0) > 0 and st.get("down", 0) > 0
+    assert 2 * (st.get("up", 0) + st.get("down", 0)) > st.get("exact", 0)
+
+
+@pytest.mark.parametrize("p", [32, 64])
+def test_block_sum_transitions_adversarial(p):
+    """Tie-prone products and exact cancellations with the transitions on."""
+    rng = random.Random(5 * p)
+    for trial in range(120):
+        ts = []
+        s_e = rng.randint(0, 8)
+        for k in range(rng.choice([8, 40, 100])):
+            kind = rng.random()
+            if kind < 0.3:
+                d = rng.randint(1, 4)
+                M = (1 << (p - 1)) | (1 << (d - 1)) | (rng.getrandbits(p - 1 - d) << d)
+                ts.append((rng.getrandbits(1), M, s_e - d + rng.randint(-1, 1)))
+            elif kind < 0.4:
+                ts.append((0, 0, 0))
+            else:
+                ts.append(_rand_t(rng, p, s_e - 3, s_e + 1))
+        got, _ = block_sum_chain(ts, p, G=rng.choice([4, 32]), transitions=True)
+        assert got == oracle_chain(ts, p), trial
