@@ -58,29 +58,27 @@ __global__ void __launch_bounds__(128, MINB) spmv_sell(PartView P, XView x, YVie
     mp_mul<L>(a, ea, (uint32_t)w >> 31, xv, ex, sx, t);
     mp_add<L>(s, t);
   };
-  // columns run two entries ahead of the fetches that use them (c1: entry
-  // j+1, c2: entry j+2 at the top of iteration j): a column load from HBM
-  // takes longer than one step
-  int c1 = 0, c2 = 0;
+  // columns run two entries ahead of the fetches that use them: a column
+  // load from HBM takes longer than one step.  cod / cev hold the column of
+  // the next odd / even entry to fetch and are reloaded IN PLACE right after
+  // their use (a rotating c1 = c2 copy made ptxas move the just-loaded
+  // register at once, stalling on the load: ~30% of a lone warp's time).
+  int cod = 0, cev = 0;
   if (len > 0) {
     fetch(0, __ldg(colp), a0, x0, w0, e0, s0);
-    if (len > 1) c1 = __ldg(colp + 32);
-    if (len > 2) c2 = __ldg(colp + 64);
+    if (len > 1) cod = __ldg(colp + 32);
+    if (len > 2) cev = __ldg(colp + 64);
   }
   for (int j = 0; j < len; j += 2) {
     if (j + 1 < len) {
-      const int c = c1;
-      c1 = c2;
-      if (j + 3 < len) c2 = __ldg(colp + 32 * (j + 3));
-      fetch(j + 1, c, a1, x1, w1, e1, s1);
+      fetch(j + 1, cod, a1, x1, w1, e1, s1);
+      if (j + 3 < len) cod = __ldg(colp + 32 * (j + 3));
     }
     step(a0, x0, w0, e0, s0);
     if (j + 1 >= len) break;
     if (j + 2 < len) {
-      const int c = c1;
-      c1 = c2;
-      if (j + 4 < len) c2 = __ldg(colp + 32 * (j + 4));
-      fetch(j + 2, c, a0, x0, w0, e0, s0);
+      fetch(j + 2, cev, a0, x0, w0, e0, s0);
+      if (j + 4 < len) cev = __ldg(colp + 32 * (j + 4));
     }
     step(a1, x1, w1, e1, s1);
   }
@@ -145,11 +143,11 @@ __global__ void __launch_bounds__(CP_THREADS, CpMinB<L>::v) spmv_sell_cp(PartVie
   };
   MP<L> s;
   s.set_zero();
-  int c1 = 0, c2 = 0;
+  int cq[2] = {0, 0};                            // next odd / even entry's column (in place)
   if (len > 0) {
     issue(0, __ldg(colp), 0);
-    if (len > 1) c1 = __ldg(colp + 32);
-    if (len > 2) c2 = __ldg(colp + 64);
+    if (len > 1) cq[1] = __ldg(colp + 32);
+    if (len > 2) cq[0] = __ldg(colp + 64);
   }
   for (int j = 0; j < len; j += 2) {
 #pragma unroll
@@ -157,10 +155,8 @@ __global__ void __launch_bounds__(CP_THREADS, CpMinB<L>::v) spmv_sell_cp(PartVie
       const int jj = j + u;
       if (jj >= len) break;
       if (jj + 1 < len) {
-        const int c = c1;
-        c1 = c2;
-        if (jj + 3 < len) c2 = __ldg(colp + 32 * (jj + 3));
-        issue(jj + 1, c, u ^ 1);
+        issue(jj + 1, cq[u ^ 1], u ^ 1);
+        if (jj + 3 < len) cq[u ^ 1] = __ldg(colp + 32 * (jj + 3));
         cp_async_wait<1>();                      // entry jj has landed
       } else {
         cp_async_wait<0>();
@@ -216,11 +212,23 @@ static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStrea
     }
   }
   // tuning knob (read per launch): MPSP_MINB = min resident blocks per SM
-  // (register cap).  Defaults measured on B200: 6 at L <= 8 (80 registers;
-  // C2 0.0385 -> 0.0332 ms, C4 A^T 0.316 -> 0.295 ms), 4 at L = 16 (128
-  // registers; C3 0.280 -> 0.239 ms), 1 at L = 32 (more spills than gain).
+  // (register cap).  Defaults measured on B200: at L <= 8, 5 (96 registers,
+  // no spills; C4 A x 0.380 -> 0.372 ms, A^T x 0.296 -> 0.279 ms) unless the
+  // whole grid is resident in one wave only at 6 (80 registers, a 28-byte
+  // spill; C2 0.0332 -> 0.0319 ms); 4 at L = 16 (128 registers; C3 0.280 ->
+  // 0.239 ms); 1 at L = 32 (more spills than gain).
   const char* vm = std::getenv("MPSP_MINB");
-  const int minb = vm ? std::atoi(vm) : (L <= 8 ? 6 : (L == 16 ? 4 : 1));
+  int minb = L == 16 ? 4 : 1;
+  if (L <= 8) {
+    static int sms = 0;
+    if (sms == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    minb = (blocks > (int64_t)sms * 5 && blocks <= (int64_t)sms * 6) ? 6 : 5;
+  }
+  if (vm) minb = std::atoi(vm);
   const unsigned nb = (unsigned)blocks;
   switch (minb) {
     case 2: spmv_sell<L, 2><<<nb, threads, 0, st>>>(P, x, y); break;
