@@ -206,11 +206,68 @@ struct WChain {
         const bool fnz = (fy != 0u) || (stk != 0u);   // fraction != 0
         const bool up_f = use && t.s == sg && LB + h - 1 >= HI;
         const bool dn_f = use && t.s != sg && LB + ek + h + 2 <= LO && LB + h - 1 >= LO / 2;
+        // dominant product (|t| >= 2^(E-1), t.e - E = dd in [0, 27]): the binade
+        // E + k of V = S u + t certified from the high-part bounds and t's top
+        // 32 bits (units 2^(E-HB)); t/u = M_t 2^dd is an integer
+        const int dd = (int)min(max(-d64, (int64_t)0), (int64_t)27);
+        const uint32_t mt = t.m[L - 1];
+        const int64_t tl = dd >= 6 ? ((int64_t)mt << (dd - 6)) : (int64_t)(mt >> (6 - dd));
+        const int64_t th = tl + (dd >= 6 ? ((int64_t)1 << (dd - 6)) : (int64_t)1);
+        const bool same = t.s == sg;
+        const int64_t vlo = same ? (int64_t)LB + tl : tl - (int64_t)LB - ek;
+        const int64_t vhi = same ? (int64_t)LB + ek + th : th - (int64_t)LB + 1;
+        const int kd = vlo > 0 ? (64 - __clzll(vlo)) - HB : 0;
+        const bool dom_f = badd && -d64 <= 27 && kd >= 1 && kd <= 26 &&
+                           vhi <= ((int64_t)1 << (HB + kd)) - 1;
 #ifdef MPSP_TRANS_MASK
-        const int mode = __shfl_sync(FULL, up_f ? 1 : (dn_f ? 2 : 0), f) & MPSP_TRANS_MASK;
+        const int mode = __shfl_sync(FULL, up_f ? 1 : (dn_f ? 2 : (dom_f ? 4 : 0)), f) & MPSP_TRANS_MASK;
 #else
-        const int mode = __shfl_sync(FULL, up_f ? 1 : (dn_f ? 2 : 0), f);
+        const int mode = __shfl_sync(FULL, up_f ? 1 : (dn_f ? 2 : (dom_f ? 4 : 0)), f);
 #endif
+        if (mode == 4) {
+          const int k = __shfl_sync(FULL, kd, f);
+          const int64_t vlof = __shfl_sync(FULL, vlo, f), vhif = __shfl_sync(FULL, vhi, f);
+          const uint32_t sgf = __shfl_sync(FULL, t.s, f);
+          if (sgf != sg) {                            // S := -S: W = |t|/u - S > 0
+#pragma unroll
+            for (int i = 0; i < N; ++i) R[i] = ~R[i];
+            inc_n<N>(R, 1u);
+          }
+          if (lane == f) {                            // W = R-sum + M_t << dd
+            uint32_t Yv[N];
+            Yv[0] = t.m[0] << dd;
+#pragma unroll
+            for (int i = 1; i < L; ++i) Yv[i] = __funnelshift_l(t.m[i - 1], t.m[i], dd);
+            Yv[L] = dd ? (t.m[L - 1] >> (32 - dd)) : 0u;
+            Yv[L + 1] = 0u;
+            add_n<N>(R, R, Yv);
+          }
+          // RN_int(W / 2^k): W mod 2^k from the lanes' low k bits (k <= 26:
+          // their sum fits 31 bits), floor(W / 2^k) = sum of the lanes'
+          // arithmetic shifts + the carry of that sum
+          const uint32_t lows = __reduce_add_sync(FULL, R[0] & ((1u << k) - 1u));
+          const uint32_t c = lows >> k;
+          const uint32_t rb = (lows >> (k - 1)) & 1u;
+          const uint32_t stk2 = (lows & ((1u << (k - 1)) - 1u)) != 0u ? 1u : 0u;
+          const uint32_t par = ((uint32_t)__popc(__ballot_sync(FULL, (R[0] >> k) & 1u)) + c) & 1u;
+          const uint32_t incr = rb & (stk2 | par);
+#pragma unroll
+          for (int i = 0; i < N - 1; ++i) R[i] = __funnelshift_r(R[i], R[i + 1], k);
+          R[N - 1] = (uint32_t)((int32_t)R[N - 1] >> k);
+          if (lane == 0) {
+            uint32_t Cv[N];
+            Cv[0] = c + incr;
+#pragma unroll
+            for (int i = 1; i < N; ++i) Cv[i] = 0u;
+            add_n<N>(R, R, Cv);
+          }
+          sg = sgf;
+          E += k;
+          Shi = (int32_t)((vlof >> k) - 1);
+          err = (int32_t)((vhif >> k) - (vlof >> k) + 3);
+          start = f + 1;
+          continue;
+        }
         if (mode != 0) {
           const int32_t LBf = __shfl_sync(FULL, LB, f);
           const int32_t hf = __shfl_sync(FULL, h, f);

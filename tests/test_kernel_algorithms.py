@@ -195,6 +195,38 @@ def block_sum_chain(ts, p, G=32, ties_exact=False, transitions=False, stats=None
             S += sum(Q[start:fail])
             nfast += cnt
             assert (1 << (p - 1)) <= S < (1 << p)
+            st_, Mt_, Et_ = blk[fail]
+            if transitions and E - Et_ < 1 and Et_ - E <= 27:
+                # dominant product (|t| >= 2^(E-1)): V = S u + t lies in a binade
+                # E + k (1 <= k <= 26) certified from the high-part bounds and
+                # t's top 32 bits; W = S +- t/u is an integer (t is on a grid
+                # >= u) and RN(V) = RN_int(W / 2^k) on the grid 2^k u
+                dd = Et_ - E
+                LBf = Shi + sum(hi(q) for q in Q[start:fail])
+                ek = err + fail
+                mt = Mt_ >> (p - 32)
+                tl = mt << (dd - 6) if dd >= 6 else mt >> (6 - dd)
+                th = tl + ((1 << (dd - 6)) if dd >= 6 else 1)
+                if st_ == sg:
+                    vlo, vhi = LBf + tl, LBf + ek + th
+                else:
+                    vlo, vhi = tl - LBf - ek, th - LBf + 1
+                k = vlo.bit_length() - HB if vlo > 0 else 0
+                if 1 <= k <= 26 and vhi <= (1 << (HB + k)) - 1:
+                    W = S + (Mt_ << dd) if st_ == sg else (Mt_ << dd) - S
+                    q = W >> k
+                    rb = (W >> (k - 1)) & 1
+                    sticky = (W & ((1 << (k - 1)) - 1)) != 0
+                    S = q + (rb & (1 if sticky else (q & 1)))
+                    sg, E = st_, E + k
+                    Shi, err = (vlo >> k) - 1, (vhi >> k) - (vlo >> k) + 3
+                    par = S & 1
+                    assert (1 << (p - 1)) <= S < (1 << p)
+                    assert Shi <= hi(S) < Shi + err
+                    if stats is not None:
+                        stats["dom"] = stats.get("dom", 0) + 1
+                    start = fail + 1
+                    continue
             if transitions and not bad[fail]:
                 LBf = Shi + sum(hi(q) for q in Q[start:fail])
                 hf = hi(Q[fail])
@@ -340,3 +372,48 @@ def test_block_sum_transitions_adversarial(p):
                 ts.append(_rand_t(rng, p, s_e - 3, s_e + 1))
         got, _ = block_sum_chain(ts, p, G=rng.choice([4, 32]), transitions=True)
         assert got == oracle_chain(ts, p), trial
+
+
+@pytest.mark.parametrize("p", [32, 64, 256])
+def test_block_sum_dominant_transitions(p):
+    """Wide exponent ranges (C4: products of exponents U[-32,32]): most exact-
+    path steps are a new product that dominates the running sum (|t| >=
+    2^(E-1)); they must be taken by the dominant-product transition, and every
+    result must be the ordered chain's - including near-cancelling opposite
+    products, exact ties on the coarser grid and jumps of up to 30 binades."""
+    rng = random.Random(17 * p)
+    st = {}
+    for trial in range(40):
+        n = rng.choice([50, 300, 900])
+        ts = []
+        for k in range(n):
+            kind = rng.random()
+            if kind < 0.08 and ts:
+                s = oracle_chain(ts, p)
+                if s[1]:
+                    # opposite sign, slightly larger: |V| small or a binade down
+                    M = s[1] + rng.randint(1, 1 << max(p - 8, 1))
+                    if M < (1 << p):
+                        ts.append((s[0] ^ 1, M, s[2]))
+                        continue
+            if kind < 0.14 and ts:
+                s = oracle_chain(ts, p)
+                if s[1]:
+                    # same or opposite sign, 2..30 binades up, low bits 0 or 10..0
+                    dd = rng.randint(2, 30)
+                    M = (1 << (p - 1)) | (rng.getrandbits(p - 1) & ~((1 << rng.randint(0, 6)) - 1))
+                    ts.append((rng.getrandbits(1), M, s[2] + dd))
+                    continue
+            ts.append(_rand_t(rng, p, -40, 40))
+        got, _ = block_sum_chain(ts, p, G=rng.choice([4, 32]), transitions=True, stats=st)
+        assert got == oracle_chain(ts, p), trial
+    assert st.get("dom", 0) > 0
+    # C4-like rows (products of values with exponents U[-32, 32]): the
+    # dominant transition takes most of what used to be exact-path steps
+    st = {}
+    for trial in range(6):
+        ts = [oracle.mul(_rand_t(rng, p, -32, 32), _rand_t(rng, p, -32, 32), p)
+              for _ in range(rng.choice([300, 1000]))]
+        got, _ = block_sum_chain(ts, p, transitions=True, stats=st)
+        assert got == oracle_chain(ts, p), ("c4-like", trial)
+    assert st.get("dom", 0) > 2 * st.get("exact", 0)
