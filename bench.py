@@ -357,6 +357,12 @@ def main():
     roof["frac_of_t_roof"] = max(t_mem, t_int) / kern_avg_s
     roof["hbm_achieved_gbs"] = bytes_local / kern_avg_s / 1e9
     roof["macs_achieved_T"] = macs_local / kern_avg_s / 1e12
+    # the algorithmic count is the schoolbook L^2 per nnz; the
+    # short product with its exactness certificate executes fewer (DESIGN.md
+    # "Product"), so frac can exceed 1: also report the IMAD pipe's own load
+    ex_per = L * L - (L - 3) * (L - 2) // 2 if L >= 4 else L * L
+    roof["executed_macs_per_nnz"] = ex_per
+    roof["frac_executed"] = (nnz_local * ex_per / kern_avg_s) / int_peak
 
     cpu = None
     if not args.no_cpu and world == 1:

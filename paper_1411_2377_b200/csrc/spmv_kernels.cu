@@ -52,11 +52,15 @@ __global__ void __launch_bounds__(128, MINB) spmv_sell(PartView P, XView x, YVie
     sx = __ldg(x.signs + col);
   };
   auto step = [&](const uint32_t (&a)[L], const uint32_t (&xv)[L], int32_t w, int32_t ex,
-                  uint32_t sx) {
+                  uint32_t sx, bool first) {
     MP<L> t;
     const int32_t ea = (int32_t)((uint32_t)w << 1) >> 1;
     mp_mul<L>(a, ea, (uint32_t)w >> 31, xv, ex, sx, t);
-    mp_add<L>(s, t);
+    if (first) {                     // RN(+0 + t) = t: the first add is a copy
+      s = t;                         // (warp-uniform: all lanes are at step j)
+    } else {
+      mp_add<L>(s, t);
+    }
   };
   // columns run two entries ahead of the fetches that use them: a column
   // load from HBM takes longer than one step.  cod / cev hold the column of
@@ -74,13 +78,13 @@ __global__ void __launch_bounds__(128, MINB) spmv_sell(PartView P, XView x, YVie
       fetch(j + 1, cod, a1, x1, w1, e1, s1);
       if (j + 3 < len) cod = __ldg(colp + 32 * (j + 3));
     }
-    step(a0, x0, w0, e0, s0);
+    step(a0, x0, w0, e0, s0, j == 0);
     if (j + 1 >= len) break;
     if (j + 2 < len) {
       fetch(j + 2, cev, a0, x0, w0, e0, s0);
       if (j + 4 < len) cev = __ldg(colp + 32 * (j + 4));
     }
-    step(a1, x1, w1, e1, s1);
+    step(a1, x1, w1, e1, s1, false);
   }
   store_y<L>(y, row, s);
 }
@@ -182,7 +186,11 @@ __global__ void __launch_bounds__(CP_THREADS, CpMinB<L>::v) spmv_sell_cp(PartVie
         const uint4 v = *sa(u, c);
         s.m[4 * c] = v.x; s.m[4 * c + 1] = v.y; s.m[4 * c + 2] = v.z; s.m[4 * c + 3] = v.w;
       }
-      mp_add<L>(s, t);
+      if (jj == 0) {
+        s = t;                                   // RN(+0 + t) = t
+      } else {
+        mp_add<L>(s, t);
+      }
     }
   }
   store_y<L>(y, row, s);
