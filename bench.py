@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--exchange", default="window", choices=["window", "allgather"],
                     help="x exchange for N > 1 (dist.py)")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--p", type=int, default=None,
+                    help="override the config's precision (e.g. 2048: the paper's solver precision)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -114,6 +116,11 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
+def workload_name(args):
+    """`C2 ax`, or `C2@p2048 ax` with a precision override."""
+    return f"{args.config}{'' if args.p is None else f'@p{args.p}'} {args.op}"
+
+
 def cpu_baseline(d, op, seconds, rows_cap=None):
     """The oracle as it stands on the host cores over a bounded row sample."""
     from oracle import run_parallel
@@ -150,7 +157,7 @@ def run_reference(args):
     if rank != 0:
         return
     import gen
-    d = gen.make(args.config, seed=args.seed)
+    d = gen.make(args.config, seed=args.seed, p=args.p)
     times, nnzs, cb = [], [], None
     for step in range(args.warmup + args.steps):
         cb = cpu_baseline(d, args.op, seconds=max(1.0, 60.0 / (args.warmup + args.steps)))
@@ -164,7 +171,7 @@ def run_reference(args):
             "ms_per_step": 1e3 * d["meta"]["nnz"] / value, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": f"u32 limbs (p={d['p']})",
             "data": "synthetic",
-            "config": {"workload": f"{args.config} {args.op}", **d["meta"]},
+            "config": {"workload": workload_name(args), **d["meta"]},
             "cpu_baseline": {**cb, "value": value},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "note": "each step is a bounded row sample of the workload; ms_per_step extrapolates "
@@ -196,7 +203,7 @@ def main():
     from paper_1411_2377_b200.dist import block_range, allgather_x, needed_window, WindowExchange
 
     t0 = time.perf_counter()
-    d = gen.make(args.config, seed=args.seed)
+    d = gen.make(args.config, seed=args.seed, p=args.p)
     t_gen = time.perf_counter() - t0
     n, p = d["n"], d["p"]
     L = p // 32
@@ -343,13 +350,16 @@ def main():
     roof["traffic"] = None
     tj = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tj) and world == 1:
-        rec = json.load(open(tj)).get(f"{args.config} {args.op}")
+        rec = json.load(open(tj)).get(workload_name(args))
         if rec:
             roof["traffic"] = rec["traffic_bytes"]
             roof["traffic_source"] = f"profiles/{rec['summary'] or rec['report']} ({rec['kernel']})"
             roof["algorithmic_bytes"] = bytes_local
     thr = int(os.environ.get("MPSP_LONG_T", "192"))
     sell = f"spmv_sell_cp<{L}>" if L == 32 and os.environ.get("MPSP_CP", "1") != "0" else f"spmv_sell<{L}>"
+    if L > 32:
+        sell = f"spmv_wide<{L // 32}> (warp per row, limbs across lanes)"
+        thr = 1 << 62
     roof["kernel"] = (sell if d["meta"]["max_row"] <= thr or args.op == "atx" else
                       f"{sell} + spmv_wrow<{L}> (concurrent streams, fork/join timed as one)")
     roof["kernel_ms"] = kern_avg_s * 1e3
@@ -360,7 +370,8 @@ def main():
     # the algorithmic count is the schoolbook L^2 per nnz; the
     # short product with its exactness certificate executes fewer (DESIGN.md
     # "Product"), so frac can exceed 1: also report the IMAD pipe's own load
-    ex_per = L * L - (L - 3) * (L - 2) // 2 if L >= 4 else L * L
+    # (p > 1024, spmv_wide: the full product plus the diagonal chunks' second MAC)
+    ex_per = (L * L - (L - 3) * (L - 2) // 2 if L >= 4 else L * L) if L <= 32 else L * L + 32 * L
     roof["executed_macs_per_nnz"] = ex_per
     roof["frac_executed"] = (nnz_local * ex_per / kern_avg_s) / int_peak
 
@@ -373,7 +384,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": f"u32 limbs (p={p})",
         "data": "synthetic",
-        "config": {"workload": f"{args.config} {args.op}", "n": n, "nnz": nnz_all, "p": p,
+        "config": {"workload": workload_name(args), "n": n, "nnz": nnz_all, "p": p,
                    "max_row": d["meta"]["max_row"], "seed": args.seed,
                    "parallelism": f"row-block x{world}" + (
                        "" if world == 1 else (" + NCCL all-gather of x" if X is None else

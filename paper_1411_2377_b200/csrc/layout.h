@@ -72,6 +72,9 @@ struct YView {
 
 // Launch the SpMV over one part on `stream`; returns a cudaError_t value.
 int launch_spmv(int L, const PartView& P, const XView& x, const YView& y, void* stream);
+// p > 1024 (L = 64, 128, 256): one warp per row over all P.nwrow rows
+// (entry-major limbs), MP arithmetic spread across the lanes (spmv_wide.cu).
+int launch_spmv_wide(int L, const PartView& P, const XView& x, const YView& y, void* stream);
 // Warp-row kernel over the P.nwrow long rows; returns a cudaError_t value.
 int launch_spmv_long(int L, const PartView& P, const XView& x, const YView& y, void* stream);
 // Row-length threshold above which a row goes to the warp-row kernel.

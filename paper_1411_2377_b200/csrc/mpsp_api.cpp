@@ -103,7 +103,9 @@ struct mpsp_csr {
 
 namespace {
 
-bool supported_L(int L) { return L == 1 || L == 2 || L == 4 || L == 8 || L == 16 || L == 32; }
+bool supported_L(int L) {
+  return L == 1 || L == 2 || L == 4 || L == 8 || L == 16 || L == 32 || L == 64 || L == 128 || L == 256;
+}
 
 // Build one part (rows [0,nrows) of a local CSR whose entry e of local row r
 // is source entry src(r, e)).
@@ -127,13 +129,15 @@ int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32
   for (auto& c : cnt) { int64_t t = c; c = acc; acc += t; }
   std::vector<int32_t> order((size_t)nrows);
   for (int64_t r = 0; r < nrows; ++r) order[(size_t)cnt[(size_t)(maxlen - (lrp[r + 1] - lrp[r]))]++] = (int32_t)r;
-  // warp rows: the rows longer than the threshold (a prefix of `order`)
-  const int64_t T = long_row_threshold();
+  // warp rows: the rows longer than the threshold (a prefix of `order`);
+  // at p > 1024 (spmv_wide) every row is a warp row, entries entry-major
+  const bool wide = L > 32;
+  const int64_t T = wide ? -1 : long_row_threshold();
   int64_t nw = 0;
   while (nw < nrows && lrp[order[(size_t)nw] + 1] - lrp[order[(size_t)nw]] > T) ++nw;
   P.nwrow = nw;
   {
-    const int64_t Tpc = std::max<int64_t>(pc_row_threshold(), T + 1);
+    const int64_t Tpc = wide ? INT64_MAX : std::max<int64_t>(pc_row_threshold(), T + 1);
     int64_t np = 0;
     while (np < nw && lrp[order[(size_t)np] + 1] - lrp[order[(size_t)np]] >= Tpc) ++np;
     P.npcrow = np;
@@ -146,7 +150,7 @@ int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32
     wptr[(size_t)i] = ew;
     wrow[(size_t)i] = r;
     wlen[(size_t)i] = (int32_t)(lrp[r + 1] - lrp[r]);
-    const int64_t cs = i < P.npcrow ? 32 * pc_spl(L) : 32;
+    const int64_t cs = wide ? 1 : (i < P.npcrow ? 32 * pc_spl(L) : 32);
     ew += (wlen[(size_t)i] + cs - 1) / cs * cs;
   }
   // SELL slices of the remaining rows
@@ -191,6 +195,10 @@ int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32
     const uint32_t* src = limbs + (size_t)k * L;
     const bool nz = src[L - 1] != 0u;
     hexp[(size_t)E] = nz ? (int32_t)(((uint32_t)signs[k] << 31) | ((uint32_t)exps[k] & 0x7fffffffu)) : 0;
+    if (wide) {
+      for (int i = 0; i < L; ++i) hl[(size_t)E * L + i] = nz ? src[i] : 0u;
+      return;
+    }
     for (int c = 0; c < NC; ++c)
       for (int w = 0; w < CW; ++w)
         hl[(size_t)(((g * NC + c) * 32 + l) * CW + w)] = nz ? src[c * CW + w] : 0u;
@@ -323,6 +331,10 @@ int do_spmv(const mpsp_csr* A, bool transpose, const uint32_t* xl, const int32_t
   XView xv{xl, xe, xs};
   YView yv{yl, ye, ys};
   const PartView pv = P.view();
+  if (L > 32) {                                      // p > 1024: warp-cooperative kernel
+    const int err = launch_spmv_wide(L, pv, xv, yv, stream);
+    return err ? cuda_fail((cudaError_t)err) : MPSP_OK;
+  }
   const bool has_pc = pv.npcrow > 0, has_w = pv.nwrow > pv.npcrow, has_s = pv.nslots > 0;
   cudaStream_t us = (cudaStream_t)stream;
   cudaError_t ce;
@@ -360,7 +372,7 @@ const char* mpsp_strerror(int code) {
   switch (code) {
     case MPSP_OK: return "ok";
     case MPSP_E_ARG: return "invalid argument (null pointer, bad size or range, misaligned)";
-    case MPSP_E_PREC: return "unsupported precision (p must be 32, 64, 128, 256, 512 or 1024)";
+    case MPSP_E_PREC: return "unsupported precision (p must be 32, 64, ..., 8192, a power of two times 32; the solvers: 128 <= p <= 1024)";
     case MPSP_E_CSR: return "invalid CSR structure (rowptr/colidx)";
     case MPSP_E_UNSORTED: return "column indices not strictly increasing within a row";
     case MPSP_E_VALUE: return "invalid value (unnormalised nonzero mantissa or |exp| > 2^29)";
@@ -601,6 +613,7 @@ namespace {
 
 int check_vec_args(int p_bits, int64_t n, const void* a, const void* b, const void* c) {
   if (!mpsp_supported_precision(p_bits) || n < 0) return n < 0 ? MPSP_E_ARG : MPSP_E_PREC;
+  if (p_bits > 1024) return MPSP_E_PREC;              // vector kernels: L <= 32
   if (n > 0 && (!a || !b || !c)) return MPSP_E_ARG;
   return MPSP_OK;
 }
@@ -684,7 +697,7 @@ int mpsp_bicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, const
   if (!A || !iters || !status || max_iter < 0) return MPSP_E_ARG;
   if (!A->has_t) return MPSP_E_NOTRANS;
   if (A->rb != 0 || A->re != A->n) return MPSP_E_ARG;   // needs the whole matrix
-  if (A->p < 128) return MPSP_E_PREC;                     // 10^50 exact in p bits
+  if (A->p < 128 || A->L > 32) return MPSP_E_PREC;       // 10^50 exact in p bits; no wide solver yet
   const int L = A->L;
   const int64_t n = A->n;
   *iters = 0;
@@ -793,7 +806,7 @@ int mpsp_gpbicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, con
                 int* status, void* cuda_stream) {
   if (!A || !iters || !status || max_iter < 0) return MPSP_E_ARG;
   if (A->rb != 0 || A->re != A->n) return MPSP_E_ARG;   // needs the whole matrix
-  if (A->p < 128) return MPSP_E_PREC;
+  if (A->p < 128 || A->L > 32) return MPSP_E_PREC;
   const int L = A->L;
   const int64_t n = A->n;
   *iters = 0;

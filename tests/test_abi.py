@@ -44,9 +44,9 @@ def test_error_codes_match_header(L):
 
 
 def test_supported_precisions(L):
-    for p in (32, 64, 128, 256, 512, 1024):
+    for p in (32, 64, 128, 256, 512, 1024, 2048, 4096, 8192):
         assert _lib.supported_precision(p)
-    for p in (0, 16, 33, 96, 2048):
+    for p in (0, 16, 33, 96, 3072, 16384):
         assert not _lib.supported_precision(p)
 
 
