@@ -99,6 +99,27 @@ int mpsp_csr_create(mpsp_csr **out, int p_bits, int64_t n,
                     int64_t row_begin, int64_t row_end, uint32_t flags);
 
 /*
+ * mpsp_dense_create - a handle for a DENSE n x n matrix: the dense MP matrix-
+ * vector product of the paper's section 3 (the Lotkin
+ * dense-vs-sparse comparison).
+ *
+ *   limbs      host uint32[n*n*L] row-major (entry (i, j) at i*n + j), the
+ *              element encoding above; zeros are all-zero limbs.
+ *   exps, signs host int32[n*n], uint8[n*n].
+ *   p_bits, row_begin, row_end, flags: as for mpsp_csr_create (n <= 46340,
+ *              so n^2 <= 2^31 - 1).
+ * mpsp_spmv / mpsp_spmv_t on the handle compute y_i = the ordered chain over
+ * ALL n columns j (zeros included; their products are +0 and leave s
+ * unchanged, so the result equals mpsp_spmv on the CSR of the nonzeros bit
+ * for bit).  The kernel reads no column indices (column = position).
+ * Errors: MPSP_E_ARG, MPSP_E_PREC, MPSP_E_CSR (n too large), MPSP_E_VALUE,
+ * MPSP_E_NOMEM, MPSP_E_CUDA.  Release with mpsp_destroy.
+ */
+int mpsp_dense_create(mpsp_csr **out, int p_bits, int64_t n,
+                      const uint32_t *limbs, const int32_t *exps, const uint8_t *signs,
+                      int64_t row_begin, int64_t row_end, uint32_t flags);
+
+/*
  * mpsp_spmv - y[i - row_begin] = chain_i(A, x) for i in [row_begin, row_end).
  *
  * All pointers are DEVICE pointers on the handle's device:

@@ -238,3 +238,24 @@ def spmv_t_cols(p, rowptr, colidx, limbs, exps, signs, x_limbs, x_exps, x_signs,
             entries.append((a, x))
         out.append(row_chain(p, entries))
     return out
+
+
+# --------------------------------------------------------------------------
+# Dense MP MV (the section-3 dense
+# vs sparse comparison; SPEC dense_mv): y_i = the ordered chain over
+# ALL n columns j of row i, zeros included.
+# --------------------------------------------------------------------------
+
+def dense_mv(p, n, limbs, exps, signs, x_limbs, x_exps, x_signs, transpose=False):
+    """y = A x (or A^T x) for a dense row-major n x n A (entry (i, j) at i*n + j)."""
+    L = p // 32
+    limbs = np.asarray(limbs, dtype=np.uint32).reshape(-1, L)
+    x = unpack_vec(x_limbs, x_exps, x_signs, p)
+    out = []
+    for i in range(n):
+        entries = []
+        for j in range(n):
+            k = j * n + i if transpose else i * n + j
+            entries.append((unpack(limbs[k], int(exps[k]), int(signs[k]), p), x[j]))
+        out.append(row_chain(p, entries))
+    return pack_vec(out, p)

@@ -21,7 +21,7 @@ ERRORS = {
 ERROR_CODES = {v: k for k, v in ERRORS.items()}
 
 # every symbol include/mpsp.h declares
-SYMBOLS = ("mpsp_csr_create", "mpsp_spmv", "mpsp_spmv_t", "mpsp_spmv_host", "mpsp_spmv_t_host",
+SYMBOLS = ("mpsp_csr_create", "mpsp_dense_create", "mpsp_spmv", "mpsp_spmv_t", "mpsp_spmv_host", "mpsp_spmv_t_host",
            "mpsp_destroy", "mpsp_strerror", "mpsp_last_cuda_error", "mpsp_csr_info",
            "mpsp_launch_count", "mpsp_imad_bench", "mpsp_supported_precision",
            "mpsp_dot", "mpsp_axpy", "mpsp_bicg", "mpsp_gpbicg", "mpsp_debug_dot_stats")
@@ -54,6 +54,8 @@ def lib() -> ctypes.CDLL:
     P, I, I64, U32 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_uint32
     L.mpsp_csr_create.argtypes = [ctypes.POINTER(P), I, I64, P, P, P, P, P, I64, I64, U32]
     L.mpsp_csr_create.restype = I
+    L.mpsp_dense_create.argtypes = [ctypes.POINTER(P), I, I64, P, P, P, I64, I64, U32]
+    L.mpsp_dense_create.restype = I
     for name in ("mpsp_spmv", "mpsp_spmv_t"):
         f = getattr(L, name)
         f.argtypes = [P, P, P, P, P, P, P, P]

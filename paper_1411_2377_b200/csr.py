@@ -89,6 +89,27 @@ class CSR:
         self._h = h
         self.transpose = transpose
 
+    @classmethod
+    def dense(cls, p: int, n: int, limbs, exps, signs, rows=None, transpose: bool = False):
+        """Handle on a DENSE row-major n x n matrix (entry (i, j) at i*n + j,
+        zeros stored as all-zero limbs): mpsp_dense_create.  spmv / spmv_t then
+        run the dense MP MV - every row's chain over all n columns."""
+        self = cls.__new__(cls)
+        self.p, self.L, self.n = int(p), int(p) // 32, int(n)
+        rb, re = (0, self.n) if rows is None else (int(rows[0]), int(rows[1]))
+        self.row_begin, self.row_end = rb, re
+        li = np.ascontiguousarray(limbs, dtype=np.uint32)
+        ex = np.ascontiguousarray(exps, dtype=np.int32)
+        sg = np.ascontiguousarray(signs, dtype=np.uint8)
+        h = ctypes.c_void_p()
+        rc = _lib.lib().mpsp_dense_create(ctypes.byref(h), self.p, self.n, _ptr(li), _ptr(ex),
+                                          _ptr(sg), rb, re,
+                                          _lib.MPSP_WITH_TRANSPOSE if transpose else 0)
+        _lib.check(rc, "mpsp_dense_create")
+        self._h = h
+        self.transpose = transpose
+        return self
+
     @property
     def rows(self) -> int:
         return self.row_end - self.row_begin

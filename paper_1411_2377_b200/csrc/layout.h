@@ -74,9 +74,12 @@ struct YView {
 int launch_spmv(int L, const PartView& P, const XView& x, const YView& y, void* stream);
 // p > 1024 (L = 64, 128, 256): one warp per row over all P.nwrow rows
 // (entry-major limbs), MP arithmetic spread across the lanes (spmv_wide.cu).
-int launch_spmv_wide(int L, const PartView& P, const XView& x, const YView& y, void* stream);
+// dense = true: mpsp_dense_create's rows (column of entry j = j, no col reads).
+int launch_spmv_wide(int L, const PartView& P, const XView& x, const YView& y, void* stream,
+                     bool dense = false);
 // Warp-row kernel over the P.nwrow long rows; returns a cudaError_t value.
-int launch_spmv_long(int L, const PartView& P, const XView& x, const YView& y, void* stream);
+int launch_spmv_long(int L, const PartView& P, const XView& x, const YView& y, void* stream,
+                     bool dense = false);
 // Row-length threshold above which a row goes to the warp-row kernel.
 int long_row_threshold();
 // Row-length threshold from which a warp row goes to spmv_pcrow.

@@ -91,6 +91,7 @@ struct mpsp_csr {
   int64_t n = 0, rb = 0, re = 0;
   uint32_t flags = 0;
   bool has_t = false;
+  bool dense = false;   // mpsp_dense_create: every row holds all n columns
   DevPart A, T;
   // fork/join for running the long-row and short-row kernels concurrently
   cudaStream_t aux = nullptr, aux2 = nullptr;
@@ -116,7 +117,7 @@ bool supported_L(int L) {
 template <class Dummy = void>
 int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32_t* lcol,
                const int64_t* srck, int64_t k0, const uint32_t* limbs, const int32_t* exps,
-               const uint8_t* signs) {
+               const uint8_t* signs, bool dense = false) {
   P.nrows = nrows;
   P.nnz = lrp[nrows] - lrp[0];
   // --- a3: stable counting sort of rows by length, descending
@@ -132,12 +133,15 @@ int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32
   // warp rows: the rows longer than the threshold (a prefix of `order`);
   // at p > 1024 (spmv_wide) every row is a warp row, entries entry-major
   const bool wide = L > 32;
-  const int64_t T = wide ? -1 : long_row_threshold();
+  // (few rows - under ~32k - cannot fill the GPU one thread per row: their
+  // chains are latency-bound, so rows over 32 entries take a warp each)
+  const char* tv = std::getenv("MPSP_LONG_T");
+  const int64_t T = (wide || dense) ? -1 : (tv || nrows >= 32768 ? long_row_threshold() : 32);
   int64_t nw = 0;
   while (nw < nrows && lrp[order[(size_t)nw] + 1] - lrp[order[(size_t)nw]] > T) ++nw;
   P.nwrow = nw;
   {
-    const int64_t Tpc = wide ? INT64_MAX : std::max<int64_t>(pc_row_threshold(), T + 1);
+    const int64_t Tpc = (wide || dense) ? INT64_MAX : std::max<int64_t>(pc_row_threshold(), T + 1);
     int64_t np = 0;
     while (np < nw && lrp[order[(size_t)np] + 1] - lrp[order[(size_t)np]] >= Tpc) ++np;
     P.npcrow = np;
@@ -331,8 +335,9 @@ int do_spmv(const mpsp_csr* A, bool transpose, const uint32_t* xl, const int32_t
   XView xv{xl, xe, xs};
   YView yv{yl, ye, ys};
   const PartView pv = P.view();
-  if (L > 32) {                                      // p > 1024: warp-cooperative kernel
-    const int err = launch_spmv_wide(L, pv, xv, yv, stream);
+  if (L > 32 || A->dense) {       // p > 1024: warp-cooperative kernel; dense: warp rows
+    const int err = L > 32 ? launch_spmv_wide(L, pv, xv, yv, stream, A->dense)
+                           : launch_spmv_long(L, pv, xv, yv, stream, true);
     return err ? cuda_fail((cudaError_t)err) : MPSP_OK;
   }
   const bool has_pc = pv.npcrow > 0, has_w = pv.nwrow > pv.npcrow, has_s = pv.nslots > 0;
@@ -391,9 +396,48 @@ int mpsp_supported_precision(int p_bits) { return p_bits > 0 && p_bits % 32 == 0
 
 int64_t mpsp_launch_count(void) { return launch_counter_get(); }
 
+static int create_impl(mpsp_csr** out, int p_bits, int64_t n, const int64_t* rowptr,
+                       const int32_t* colidx, const uint32_t* limbs, const int32_t* exps,
+                       const uint8_t* signs, int64_t row_begin, int64_t row_end, uint32_t flags,
+                       bool dense);
+
 int mpsp_csr_create(mpsp_csr** out, int p_bits, int64_t n, const int64_t* rowptr,
                     const int32_t* colidx, const uint32_t* limbs, const int32_t* exps,
                     const uint8_t* signs, int64_t row_begin, int64_t row_end, uint32_t flags) {
+  return create_impl(out, p_bits, n, rowptr, colidx, limbs, exps, signs, row_begin, row_end, flags,
+                     false);
+}
+
+int mpsp_dense_create(mpsp_csr** out, int p_bits, int64_t n, const uint32_t* limbs,
+                      const int32_t* exps, const uint8_t* signs, int64_t row_begin,
+                      int64_t row_end, uint32_t flags) {
+  if (!out) return MPSP_E_ARG;
+  *out = nullptr;
+  if (n < 0 || row_begin < 0 || row_end < row_begin || row_end > n) return MPSP_E_ARG;
+  if (n > 46340) return MPSP_E_CSR;                       // n^2 entries <= 2^31-1
+  if (n > 0 && (!limbs || !exps || !signs)) return MPSP_E_ARG;
+  // the full pattern: row i holds columns 0..n-1 in order (entry i*n + j)
+  std::vector<int64_t> rp;
+  std::vector<int32_t> ci;
+  try {
+    rp.resize((size_t)n + 1);
+    ci.resize((size_t)(n * n));
+  } catch (const std::bad_alloc&) {
+    return MPSP_E_NOMEM;
+  }
+  for (int64_t i = 0; i <= n; ++i) rp[(size_t)i] = i * n;
+  parallel_for(n, [&](int64_t i0, int64_t i1) {
+    for (int64_t i = i0; i < i1; ++i)
+      for (int64_t j = 0; j < n; ++j) ci[(size_t)(i * n + j)] = (int32_t)j;
+  });
+  return create_impl(out, p_bits, n, rp.data(), ci.data(), limbs, exps, signs, row_begin, row_end,
+                     flags, true);
+}
+
+static int create_impl(mpsp_csr** out, int p_bits, int64_t n, const int64_t* rowptr,
+                       const int32_t* colidx, const uint32_t* limbs, const int32_t* exps,
+                       const uint8_t* signs, int64_t row_begin, int64_t row_end, uint32_t flags,
+                       bool dense) {
   if (!out) return MPSP_E_ARG;
   *out = nullptr;
   if (n < 0 || !rowptr || row_begin < 0 || row_end < row_begin || row_end > n) return MPSP_E_ARG;
@@ -437,6 +481,7 @@ int mpsp_csr_create(mpsp_csr** out, int p_bits, int64_t n, const int64_t* rowptr
   if (!H) return MPSP_E_NOMEM;
   H->dev = dev; H->p = p_bits; H->L = L; H->n = n; H->rb = row_begin; H->re = row_end;
   H->flags = flags;
+  H->dense = dense;
   const int64_t nrows = row_end - row_begin;
   int rc = MPSP_OK;
   // ---- part A: rows [rb, re)
@@ -444,7 +489,7 @@ int mpsp_csr_create(mpsp_csr** out, int p_bits, int64_t n, const int64_t* rowptr
     std::vector<int64_t> lrp((size_t)nrows + 1);
     const int64_t k0 = rowptr[row_begin];
     for (int64_t r = 0; r <= nrows; ++r) lrp[(size_t)r] = rowptr[row_begin + r] - k0;
-    rc = build_part(H->A, L, nrows, lrp.data(), colidx + k0, nullptr, k0, limbs, exps, signs);
+    rc = build_part(H->A, L, nrows, lrp.data(), colidx + k0, nullptr, k0, limbs, exps, signs, dense);
   }
   // ---- a2: transpose (stable counting sort on column), rows [rb, re) of A^T
   if (rc == MPSP_OK && (flags & MPSP_WITH_TRANSPOSE)) {
@@ -468,7 +513,8 @@ int mpsp_csr_create(mpsp_csr** out, int p_bits, int64_t n, const int64_t* rowptr
       }
       std::vector<int64_t> lrp((size_t)nrows + 1);
       for (int64_t r = 0; r <= nrows; ++r) lrp[(size_t)r] = tcnt[(size_t)(row_begin + r)] - t0;
-      rc = build_part(H->T, L, nrows, lrp.data(), tcol.data(), tsrc.data(), 0, limbs, exps, signs);
+      rc = build_part(H->T, L, nrows, lrp.data(), tcol.data(), tsrc.data(), 0, limbs, exps, signs,
+                      dense);
     } catch (const std::bad_alloc&) {
       rc = MPSP_E_NOMEM;
     }

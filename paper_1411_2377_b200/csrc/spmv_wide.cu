@@ -357,7 +357,7 @@ __device__ __forceinline__ void load_k(const uint32_t* __restrict__ p, uint32_t 
 
 // One warp per row (the part's rows are all "warp rows", longest first);
 // entries entry-major: entry E's L limbs at limbs[E*L ..].
-template <int K>
+template <int K, bool DENSE>
 __global__ void __launch_bounds__(32 * WARPS) spmv_wide(PartView P, XView x, YView y) {
   constexpr int L = 32 * K;
   extern __shared__ uint32_t wsm[];
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(32 * WARPS) spmv_wide(PartView P, XView x, YVi
   uint32_t nsx = 0u;
   auto fetch = [&](int j) {
     const int64_t e = e0 + j;
-    const int col = __ldg(P.col + e);
+    const int col = DENSE ? j : __ldg(P.col + e);   // dense rows: column = position
     nw = __ldg(P.expw + e);
     load_k<K>(P.limbs + e * L + lane * K, na);
     load_k<K>(x.limbs + (int64_t)col * L + lane * K, nx);
@@ -410,31 +410,35 @@ __global__ void __launch_bounds__(32 * WARPS) spmv_wide(PartView P, XView x, YVi
   }
 }
 
-template <int K>
+template <int K, bool DENSE>
 int launch(const PartView& P, const XView& x, const YView& y, cudaStream_t st) {
   if (P.nwrow <= 0) return 0;
   constexpr int L = 32 * K;
   const size_t smem = (size_t)WARPS * 8 * L * 4;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(spmv_wide<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(spmv_wide<K, DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
     attr = true;
   }
   const int64_t blocks = (P.nwrow + WARPS - 1) / WARPS;
-  spmv_wide<K><<<(unsigned)blocks, 32 * WARPS, smem, st>>>(P, x, y);
+  spmv_wide<K, DENSE><<<(unsigned)blocks, 32 * WARPS, smem, st>>>(P, x, y);
   launch_counter_add(1);
   return (int)cudaGetLastError();
 }
 
 }  // namespace wide
 
-int launch_spmv_wide(int L, const PartView& P, const XView& x, const YView& y, void* stream) {
+int launch_spmv_wide(int L, const PartView& P, const XView& x, const YView& y, void* stream,
+                     bool dense) {
   cudaStream_t st = (cudaStream_t)stream;
-  switch (L) {
-    case 64: return wide::launch<2>(P, x, y, st);
-    case 128: return wide::launch<4>(P, x, y, st);
-    case 256: return wide::launch<8>(P, x, y, st);
+  switch (L * 2 + (dense ? 1 : 0)) {
+    case 128: return wide::launch<2, false>(P, x, y, st);
+    case 129: return wide::launch<2, true>(P, x, y, st);
+    case 256: return wide::launch<4, false>(P, x, y, st);
+    case 257: return wide::launch<4, true>(P, x, y, st);
+    case 512: return wide::launch<8, false>(P, x, y, st);
+    case 513: return wide::launch<8, true>(P, x, y, st);
     default: return (int)cudaErrorInvalidValue;
   }
 }

@@ -81,14 +81,18 @@ __device__ __forceinline__ void wload(const PartView& P, const XView& x, int64_t
   E.sx = __ldg(x.signs + col);
 }
 
+// DENSE (mpsp_dense_create): every row holds all n columns in order, so the
+// column of entry j is j itself - no index array is read.
+template <bool DENSE = false>
 __device__ __forceinline__ int wcol(const PartView& P, int64_t e0, int jb, int len, int lane) {
+  if constexpr (DENSE) return (jb + lane < len) ? jb + lane : 0;
   return (jb + lane < len) ? __ldg(P.col + e0 + jb + lane) : 0;
 }
 
 #ifndef MPSP_WROW_MINB
 #define MPSP_WROW_MINB 1
 #endif
-template <int L>
+template <int L, bool DENSE = false>
 __global__ void __launch_bounds__(128, (L <= 8 ? MPSP_WROW_MINB : 1)) spmv_wrow(PartView P, XView x, YView y) {
   const int64_t w = P.npcrow + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
@@ -102,10 +106,10 @@ __global__ void __launch_bounds__(128, (L <= 8 ? MPSP_WROW_MINB : 1)) spmv_wrow(
   WEntry<L> nxt;
   int cnext = 0;                      // columns of the block after the prefetched one
   if (WPrefetch<L>::on) {
-    wload<L>(P, x, e0, 0, len, lane, wcol(P, e0, 0, len, lane), nxt);
-    cnext = wcol(P, e0, 32, len, lane);
+    wload<L>(P, x, e0, 0, len, lane, wcol<DENSE>(P, e0, 0, len, lane), nxt);
+    cnext = wcol<DENSE>(P, e0, 32, len, lane);
   } else {
-    cnext = wcol(P, e0, 0, len, lane);
+    cnext = wcol<DENSE>(P, e0, 0, len, lane);
   }
   for (int jb = 0; jb < len; jb += 32) {
     MP<L> t;
@@ -115,11 +119,11 @@ __global__ void __launch_bounds__(128, (L <= 8 ? MPSP_WROW_MINB : 1)) spmv_wrow(
         cur = nxt;
         if (jb + 32 < len) {
           wload<L>(P, x, e0, jb + 32, len, lane, cnext, nxt);
-          cnext = wcol(P, e0, jb + 64, len, lane);
+          cnext = wcol<DENSE>(P, e0, jb + 64, len, lane);
         }
       } else {
         wload<L>(P, x, e0, jb, len, lane, cnext, cur);
-        cnext = wcol(P, e0, jb + 32, len, lane);
+        cnext = wcol<DENSE>(P, e0, jb + 32, len, lane);
       }
       const int32_t ea = (int32_t)((uint32_t)cur.w << 1) >> 1;
       mp_mul<L>(cur.a, ea, (uint32_t)cur.w >> 31, cur.x, cur.ex, cur.sx, t);
@@ -373,12 +377,16 @@ __global__ void __launch_bounds__(32 * (1 + pc_spl(L))) spmv_pcrow(PartView P, X
 }
 
 template <int L>
-static int launch_wrow_L(const PartView& P, const XView& x, const YView& y, cudaStream_t st) {
+static int launch_wrow_L(const PartView& P, const XView& x, const YView& y, cudaStream_t st,
+                         bool dense) {
   const int64_t nw = P.nwrow - P.npcrow;
   if (nw <= 0) return 0;
   const int threads = 128;
   const int64_t blocks = (nw * 32 + threads - 1) / threads;
-  spmv_wrow<L><<<(unsigned)blocks, threads, 0, st>>>(P, x, y);
+  if (dense)
+    spmv_wrow<L, true><<<(unsigned)blocks, threads, 0, st>>>(P, x, y);
+  else
+    spmv_wrow<L><<<(unsigned)blocks, threads, 0, st>>>(P, x, y);
   launch_counter_add(1);
   return (int)cudaGetLastError();
 }
@@ -400,15 +408,16 @@ static int launch_pcrow_L(const PartView& P, const XView& x, const YView& y, cud
   return (int)cudaGetLastError();
 }
 
-int launch_spmv_long(int L, const PartView& P, const XView& x, const YView& y, void* stream) {
+int launch_spmv_long(int L, const PartView& P, const XView& x, const YView& y, void* stream,
+                     bool dense) {
   cudaStream_t st = (cudaStream_t)stream;
   switch (L) {
-    case 1: return launch_wrow_L<1>(P, x, y, st);
-    case 2: return launch_wrow_L<2>(P, x, y, st);
-    case 4: return launch_wrow_L<4>(P, x, y, st);
-    case 8: return launch_wrow_L<8>(P, x, y, st);
-    case 16: return launch_wrow_L<16>(P, x, y, st);
-    case 32: return launch_wrow_L<32>(P, x, y, st);
+    case 1: return launch_wrow_L<1>(P, x, y, st, dense);
+    case 2: return launch_wrow_L<2>(P, x, y, st, dense);
+    case 4: return launch_wrow_L<4>(P, x, y, st, dense);
+    case 8: return launch_wrow_L<8>(P, x, y, st, dense);
+    case 16: return launch_wrow_L<16>(P, x, y, st, dense);
+    case 32: return launch_wrow_L<32>(P, x, y, st, dense);
     default: return (int)cudaErrorInvalidValue;
   }
 }
