@@ -60,6 +60,20 @@ __device__ __forceinline__ uint32_t ripple(bool g, bool p, int lane, uint32_t* c
   return (C >> lane) & 1u;
 }
 
+// (acc64 : c2) += a*b with the low two words held as ONE 64-bit register
+// pair: IMAD.WIDE.U32 accumulates in place (three separate 32-bit words made
+// ptxas copy them into a fresh aligned pair before every multiply-add).
+__device__ __forceinline__ void mac64(uint64_t& acc, uint32_t& c2, uint32_t a, uint32_t b) {
+  asm("{\n\t.reg .u32 lo, hi;\n\t"
+      "mov.b64 {lo, hi}, %0;\n\t"
+      "mad.lo.cc.u32 lo, %2, %3, lo;\n\t"
+      "madc.hi.cc.u32 hi, %2, %3, hi;\n\t"
+      "addc.u32 %1, %1, 0;\n\t"
+      "mov.b64 %0, {lo, hi};\n\t}"
+      : "+l"(acc), "+r"(c2)
+      : "r"(a), "r"(b));
+}
+
 template <int K>
 __device__ __forceinline__ bool wzero(const WMP<K>& v) {
   return __shfl_sync(FULL, v.m[K - 1], 31) == 0u;
@@ -105,9 +119,10 @@ __device__ __forceinline__ void wmul(const uint32_t (&a)[K], int32_t ea, uint32_
   }
   __syncwarp();
   // column sums: lo[u] = column lane + 32u, hi[u] = column lane + 32u + L
-  uint32_t lo0[K], lo1[K], lo2[K], hi0[K], hi1[K], hi2[K];
+  uint64_t lo[K], hi[K];
+  uint32_t lo2[K], hi2[K];
 #pragma unroll
-  for (int u = 0; u < K; ++u) { lo0[u] = lo1[u] = lo2[u] = hi0[u] = hi1[u] = hi2[u] = 0u; }
+  for (int u = 0; u < K; ++u) { lo[u] = hi[u] = 0u; lo2[u] = hi2[u] = 0u; }
 #pragma unroll
   for (int v = 0; v < K; ++v) {                    // i in [32v, 32v + 32)
 #pragma unroll 4
@@ -118,14 +133,14 @@ __device__ __forceinline__ void wmul(const uint32_t (&a)[K], int32_t ea, uint32_
       for (int u = 0; u < K; ++u) {
         const int c = lane + 32 * u;
         if (u > v) {                               // i <= c: column c
-          mac3(lo0[u], lo1[u], lo2[u], ai, sX[c - i]);
+          mac64(lo[u], lo2[u], ai, sX[c - i]);
         } else if (u < v) {                        // i > c: column c + L
-          mac3(hi0[u], hi1[u], hi2[u], ai, sX[c + L - i]);
+          mac64(hi[u], hi2[u], ai, sX[c + L - i]);
         } else {                                   // the diagonal chunk: both
           const bool l = ii <= lane;
           const uint32_t xv = sX[l ? c - i : c + L - i];
-          mac3(lo0[u], lo1[u], lo2[u], ai, l ? xv : 0u);
-          mac3(hi0[u], hi1[u], hi2[u], ai, l ? 0u : xv);
+          mac64(lo[u], lo2[u], ai, l ? xv : 0u);
+          mac64(hi[u], hi2[u], ai, l ? 0u : xv);
         }
       }
     }
@@ -136,8 +151,8 @@ __device__ __forceinline__ void wmul(const uint32_t (&a)[K], int32_t ea, uint32_
 #pragma unroll
   for (int u = 0; u < K; ++u) {
     const int c = lane + 32 * u;
-    cs0[c] = lo0[u]; cs1[c] = lo1[u]; cs2[c] = lo2[u];
-    cs0[c + L] = hi0[u]; cs1[c + L] = hi1[u]; cs2[c + L] = hi2[u];
+    cs0[c] = (uint32_t)lo[u]; cs1[c] = (uint32_t)(lo[u] >> 32); cs2[c] = lo2[u];
+    cs0[c + L] = (uint32_t)hi[u]; cs1[c + L] = (uint32_t)(hi[u] >> 32); cs2[c + L] = hi2[u];
   }
   __syncwarp();
   // limbs [2Kj, 2Kj + 2K) of the exact product P = sum_c col_c 2^(32c)
