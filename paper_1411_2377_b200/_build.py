@@ -17,7 +17,7 @@ BUILD = os.path.join(PKG, "build")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["spmv_kernels.cu", "spmv_wrow.cu", "spmv_wide.cu", "krylov.cu", "mpsp_api.cpp"]
+SOURCES = ["spmv_kernels.cu", "spmv_wrow.cu", "spmv_wide.cu", "krylov.cu", "krylov_wide.cu", "mpsp_api.cpp"]
 
 
 def nvcc() -> str:

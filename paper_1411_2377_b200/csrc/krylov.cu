@@ -628,7 +628,8 @@ int krylov_dot(int L, int64_t n, const VecIn& u, const VecIn& v, const YView& ou
     case 8: return KrylovOps<8>::dot(n, u, v, out, stop, st, work);
     case 16: return KrylovOps<16>::dot(n, u, v, out, stop, st, work);
     case 32: return KrylovOps<32>::dot(n, u, v, out, stop, st, work);
-    default: return (int)cudaErrorInvalidValue;
+    default: return L > 32 ? krylov_wide_dot(L, n, u, v, out, stop, stream, work)
+                           : (int)cudaErrorInvalidValue;
   }
 }
 
@@ -649,7 +650,7 @@ size_t krylov_dot_work_bytes(int L, int64_t n) {
     case 8: return KrylovOps<8>::bytes(n);
     case 16: return KrylovOps<16>::bytes(n);
     case 32: return KrylovOps<32>::bytes(n);
-    default: return 0;
+    default: return L > 32 ? krylov_wide_dot_work_bytes(L, n) : 0;
   }
 }
 
@@ -663,7 +664,8 @@ int krylov_axpy(int L, int64_t n, const VecIn& al, int neg, const VecIn& x, cons
     case 8: return KrylovOps<8>::axpy(n, al, neg, x, y, z, stop, st);
     case 16: return KrylovOps<16>::axpy(n, al, neg, x, y, z, stop, st);
     case 32: return KrylovOps<32>::axpy(n, al, neg, x, y, z, stop, st);
-    default: return (int)cudaErrorInvalidValue;
+    default: return L > 32 ? krylov_wide_axpy(L, n, al, neg, x, y, z, stop, stream)
+                           : (int)cudaErrorInvalidValue;
   }
 }
 
@@ -674,7 +676,7 @@ int krylov_scalar(int L, const YView& S, int* fl, int op, void* stream) {
     case 8: return KrylovOps<8>::scalar(S, fl, op, st);
     case 16: return KrylovOps<16>::scalar(S, fl, op, st);
     case 32: return KrylovOps<32>::scalar(S, fl, op, st);
-    default: return (int)cudaErrorInvalidValue;
+    default: return L > 32 ? krylov_wide_scalar(L, S, fl, op, stream) : (int)cudaErrorInvalidValue;
   }
 }
 

@@ -1,0 +1,573 @@
+// krylov_wide.cu - the BiCG / GPBiCG building blocks at p > 1024 (L = 64,
+// 128, 256; the paper runs its solvers at 2048 bits
+// and more), on warp-distributed values
+// (wide_mp.cuh).  Same operations and readings as krylov.cu:
+//   dot   : s = RN(s + RN(u_k v_k)), k ascending, from +0.  Products in
+//           parallel (a warp per element), then ONE warp walks the ordered
+//           chain of adds (a sequential chain; no speculation at these L yet).
+//   axpy  : z_k = RN(y_k + RN(+-alpha x_k)), a warp per element.
+//   scalar: the solver's scalar steps (krylov.cu bicg_scalar ops 0-8) in one
+//           warp: RN division by restoring long division (p+4 quotient bits,
+//           sticky, one rounding), RN square root digit by digit, exact
+//           comparison - the big integers spread over the lanes (W words per
+//           lane), carries and borrows resolved by the ballot ripple.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "wide_mp.cuh"
+
+namespace mpsp {
+namespace wide {
+
+// ------------------------------------------------------------ big integers
+// lane j holds words jW .. jW+W-1 (little endian over the warp)
+
+template <int W>
+__device__ __forceinline__ bool wi_lt(const uint32_t (&a)[W], const uint32_t (&b)[W]) {
+  int cmp = 0;
+#pragma unroll
+  for (int i = W - 1; i >= 0; --i)
+    if (cmp == 0 && a[i] != b[i]) cmp = a[i] > b[i] ? 1 : -1;
+  const unsigned ne = __ballot_sync(FULL, cmp != 0);
+  return ne ? (__shfl_sync(FULL, cmp, 31 - __clz(ne)) < 0) : false;
+}
+
+// a += b (carry out of the top dropped)
+template <int W>
+__device__ __forceinline__ void wi_add(uint32_t (&a)[W], const uint32_t (&b)[W], int lane) {
+  uint32_t c = 0u;
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    const uint64_t v = (uint64_t)a[i] + b[i] + c;
+    a[i] = (uint32_t)v;
+    c = (uint32_t)(v >> 32);
+  }
+  inc_n<W>(a, ripple(c != 0u, all_ones<W>(a), lane, nullptr));
+}
+
+// a -= b (a >= b): a + ~b + 1
+template <int W>
+__device__ __forceinline__ void wi_sub(uint32_t (&a)[W], const uint32_t (&b)[W], int lane) {
+  uint32_t c = lane == 0 ? 1u : 0u;
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    const uint64_t v = (uint64_t)a[i] + (~b[i]) + c;
+    a[i] = (uint32_t)v;
+    c = (uint32_t)(v >> 32);
+  }
+  inc_n<W>(a, ripple(c != 0u, all_ones<W>(a), lane, nullptr));
+}
+
+// a += 2^pos
+template <int W>
+__device__ __forceinline__ void wi_add_bit(uint32_t (&a)[W], int pos, int lane) {
+  uint32_t b[W];
+#pragma unroll
+  for (int i = 0; i < W; ++i) b[i] = (lane * W + i == (pos >> 5)) ? (1u << (pos & 31)) : 0u;
+  wi_add<W>(a, b, lane);
+}
+
+template <int W>
+__device__ __forceinline__ void wi_shl1(uint32_t (&a)[W], int lane) {
+  const uint32_t below = __shfl_up_sync(FULL, a[W - 1], 1);
+  const uint32_t lo = lane ? below : 0u;
+#pragma unroll
+  for (int i = W - 1; i > 0; --i) a[i] = __funnelshift_l(a[i - 1], a[i], 1);
+  a[0] = __funnelshift_l(lo, a[0], 1);
+}
+
+template <int W>
+__device__ __forceinline__ void wi_shr1(uint32_t (&a)[W], int lane) {
+  const uint32_t above = __shfl_down_sync(FULL, a[0], 1);
+  const uint32_t hi = lane < 31 ? above : 0u;
+#pragma unroll
+  for (int i = 0; i < W - 1; ++i) a[i] = __funnelshift_r(a[i], a[i + 1], 1);
+  a[W - 1] = __funnelshift_r(a[W - 1], hi, 1);
+}
+
+template <int W>
+__device__ __forceinline__ bool wi_nonzero(const uint32_t (&a)[W]) {
+  uint32_t o = 0u;
+#pragma unroll
+  for (int i = 0; i < W; ++i) o |= a[i];
+  return __ballot_sync(FULL, o != 0u) != 0u;
+}
+
+// bit length (0 for zero)
+template <int W>
+__device__ __forceinline__ int wi_bitlen(const uint32_t (&a)[W], int lane) {
+  int b = 0;
+#pragma unroll
+  for (int i = 0; i < W; ++i)
+    if (a[i]) b = 32 * (lane * W + i) + 32 - __clz(a[i]);
+  return (int)__reduce_max_sync(FULL, (unsigned)b);
+}
+
+// a <<= s (any s >= 0; bits beyond 32*32W dropped) through shared memory
+// sm: at least 32W + 1 words
+template <int W>
+__device__ __forceinline__ void wi_shl(uint32_t (&a)[W], int s, uint32_t* sm, int lane) {
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < W; ++i) sm[1 + lane * W + i] = a[i];
+  if (lane == 0) sm[0] = 0u;
+  __syncwarp();
+  const int q = s >> 5;
+  const uint32_t r = (uint32_t)s & 31u;
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    const int k = lane * W + i - q;                // source word (sm index k + 1)
+    const uint32_t hw = k >= 0 ? sm[1 + k] : 0u, lw = k >= 1 ? sm[k] : 0u;
+    a[i] = __funnelshift_l(lw, hw, r);
+  }
+  __syncwarp();
+}
+
+// element layout (K limbs per lane) <-> big integer layout (W words per lane)
+template <int K, int W>
+__device__ __forceinline__ void to_wi(const uint32_t (&m)[K], uint32_t (&a)[W], uint32_t* sm,
+                                      int lane) {
+  constexpr int L = 32 * K;
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < K; ++i) sm[lane * K + i] = m[i];
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    const int k = lane * W + i;
+    a[i] = k < L ? sm[k] : 0u;
+  }
+  __syncwarp();
+}
+
+// o = RN_p(N 2^f), N > 0 (the p-bit rounding of krylov.cu round_int)
+template <int K, int W>
+__device__ void wi_round(const uint32_t (&N)[W], int32_t f, uint32_t* sm, int lane, WMP<K>& o) {
+  constexpr int L = 32 * K, P = 32 * L;
+  const int b = wi_bitlen<W>(N, lane);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < W; ++i) sm[lane * W + i] = N[i];
+  if (lane == 0) { sm[32 * W] = 0u; sm[32 * W + 1] = 0u; }
+  __syncwarp();
+  uint32_t cy = 0u;
+  if (b > P) {
+    const int sh = b - P;                          // bits dropped below the LSB
+    const int q = sh >> 5;
+    const uint32_t r = (uint32_t)sh & 31u;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const int m = lane * K + i;
+      o.m[i] = __funnelshift_r(sm[q + m], sm[q + m + 1], r);
+    }
+    const int rbpos = sh - 1;
+    const uint32_t rb = (sm[rbpos >> 5] >> (rbpos & 31)) & 1u;
+    uint32_t orr = 0u;                             // bits [0, sh-1)
+    for (int k = lane; k < (rbpos >> 5); k += 32) orr |= sm[k];
+    if (lane == 0) orr |= sm[rbpos >> 5] & ((1u << (rbpos & 31)) - 1u);
+    const bool sticky = __ballot_sync(FULL, orr != 0u) != 0u;
+    const uint32_t lsb = __shfl_sync(FULL, o.m[0], 0) & 1u;
+    __syncwarp();
+    cy = wround<K>(o.m, rb & ((sticky ? 1u : 0u) | lsb), lane);
+    if (cy && lane == 31) o.m[K - 1] = 0x80000000u;
+  } else {
+    const int s = P - b;                           // exact left shift
+    const int q = s >> 5;
+    const uint32_t r = (uint32_t)s & 31u;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const int k = lane * K + i - q;
+      const uint32_t hw = k >= 0 ? sm[k] : 0u, lw = k >= 1 ? sm[k - 1] : 0u;
+      o.m[i] = __funnelshift_l(lw, hw, r);
+    }
+    __syncwarp();
+  }
+  o.e = f + b + (int32_t)cy;
+}
+
+// q = RN(a / b), b != 0 (krylov.cu mp_div: restoring division, K = p+3)
+template <int K>
+__device__ void wdiv(const WMP<K>& a, const WMP<K>& b, WMP<K>& q, uint32_t* sm, int lane) {
+  constexpr int L = 32 * K, W = K + 1, KD = 32 * L + 3;
+  if (wzero<K>(a) || wzero<K>(b)) { wset_zero<K>(q); return; }
+  uint32_t R[W], D[W], Q[W];
+  to_wi<K, W>(a.m, R, sm, lane);
+  to_wi<K, W>(b.m, D, sm, lane);
+#pragma unroll
+  for (int i = 0; i < W; ++i) Q[i] = 0u;
+  for (int i = 0; i <= KD; ++i) {
+    wi_shl1<W>(Q, lane);
+    if (!wi_lt<W>(R, D)) {
+      wi_sub<W>(R, D, lane);
+      if (lane == 0) Q[0] |= 1u;
+    }
+    wi_shl1<W>(R, lane);
+  }
+  const bool nz = wi_nonzero<W>(R);
+  wi_shl1<W>(Q, lane);
+  if (lane == 0 && nz) Q[0] |= 1u;
+  wi_round<K, W>(Q, a.e - b.e - KD - 1, sm, lane, q);
+  q.s = a.s ^ b.s;
+}
+
+// r = RN(sqrt(a)), a >= 0 (krylov.cu mp_sqrt: digit by digit, K = p/2 + 3)
+template <int K>
+__device__ void wsqrt(const WMP<K>& a, WMP<K>& r, uint32_t* sm, int lane) {
+  constexpr int L = 32 * K, W = 2 * K + 1, KS = 16 * L + 3;
+  if (wzero<K>(a)) { wset_zero<K>(r); return; }
+  int32_t e = a.e - 32 * L;
+  uint32_t X[W], Rt[W], T[W];
+  to_wi<K, W>(a.m, X, sm, lane);
+#pragma unroll
+  for (int i = 0; i < W; ++i) Rt[i] = 0u;
+  if (e & 1) { wi_shl1<W>(X, lane); e -= 1; }
+  wi_shl<W>(X, 2 * KS, sm, lane);
+  int pos = (wi_bitlen<W>(X, lane) - 1) & ~1;      // highest power of 4 <= X
+  for (; pos >= 0; pos -= 2) {
+#pragma unroll
+    for (int i = 0; i < W; ++i) T[i] = Rt[i];
+    wi_add_bit<W>(T, pos, lane);                     // T = res + bit
+    wi_shr1<W>(Rt, lane);
+    if (!wi_lt<W>(X, T)) {
+      wi_sub<W>(X, T, lane);
+      wi_add_bit<W>(Rt, pos, lane);
+    }
+  }
+  const bool nz = wi_nonzero<W>(X);
+  wi_shl1<W>(Rt, lane);
+  if (lane == 0 && nz) Rt[0] |= 1u;
+  wi_round<K, W>(Rt, e / 2 - KS - 1, sm, lane, r);
+  r.s = 0u;
+}
+
+// exact comparison: -1, 0, 1 (warp-uniform)
+template <int K>
+__device__ int wcmp(const WMP<K>& a, const WMP<K>& b) {
+  const bool az = wzero<K>(a), bz = wzero<K>(b);
+  const int ga = az ? 0 : (a.s ? -1 : 1);
+  const int gb = bz ? 0 : (b.s ? -1 : 1);
+  if (ga != gb) return ga < gb ? -1 : 1;
+  if (ga == 0) return 0;
+  int c = (a.e > b.e) - (a.e < b.e);
+  if (c == 0) {
+    c = wi_lt<K>(b.m, a.m) ? 1 : (wi_lt<K>(a.m, b.m) ? -1 : 0);
+  }
+  return ga > 0 ? c : -c;
+}
+
+// ----------------------------------------------------------- load / store
+template <int K>
+__device__ __forceinline__ void wload(const VecIn& v, int64_t k, int lane, WMP<K>& a) {
+  constexpr int L = 32 * K;
+  load_k<K>(v.limbs + k * L + lane * K, a.m);
+  a.e = __ldg(v.exps + k);
+  a.s = __ldg(v.signs + k);
+  if (wzero<K>(a)) { a.e = 0; a.s = 0u; }
+}
+
+template <int K>
+__device__ __forceinline__ void wstore(const YView& y, int64_t k, int lane, const WMP<K>& a) {
+  constexpr int L = 32 * K;
+  const bool z = wzero<K>(a);
+#pragma unroll
+  for (int i = 0; i < K; ++i) y.limbs[k * L + lane * K + i] = a.m[i];
+  if (lane == 0) {
+    y.exps[k] = z ? 0 : a.e;
+    y.signs[k] = z ? (uint8_t)0 : (uint8_t)a.s;
+  }
+}
+
+// ------------------------------------------------------------------ kernels
+constexpr int KW = 4;                                // warps per block
+
+// t_k = RN(u_k v_k) into the scratch vector P (ABI element layout)
+template <int K>
+__global__ void __launch_bounds__(32 * KW) wdot_products(int64_t n, VecIn u, VecIn v, YView P,
+                                                         const int* stop) {
+  constexpr int L = 32 * K;
+  if (stop && *stop) return;
+  extern __shared__ uint32_t wsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* sA = wsm + warp * 8 * L;
+  for (int64_t k = (int64_t)blockIdx.x * KW + warp; k < n; k += (int64_t)gridDim.x * KW) {
+    WMP<K> a, b, t;
+    wload<K>(u, k, lane, a);
+    wload<K>(v, k, lane, b);
+    wmul<K>(a.m, a.e, a.s, b.m, b.e, b.s, sA, sA + L, sA + 2 * L, lane, t);
+    wstore<K>(P, k, lane, t);
+    __syncwarp();
+  }
+}
+
+// out = the ordered chain of adds over P[0..n)
+template <int K>
+__global__ void __launch_bounds__(32) wdot_chain(int64_t n, VecIn P, YView out, const int* stop) {
+  constexpr int L = 32 * K;
+  if (stop && *stop) return;
+  extern __shared__ uint32_t wsm[];
+  const int lane = threadIdx.x & 31;
+  WMP<K> s, t, nx;
+  wset_zero<K>(s);
+  if (n > 0) wload<K>(P, 0, lane, nx);
+  for (int64_t k = 0; k < n; ++k) {
+    t = nx;
+    if (k + 1 < n) wload<K>(P, k + 1, lane, nx);
+    wadd<K>(s, t, wsm, lane);
+    __syncwarp();
+  }
+  wstore<K>(out, 0, lane, s);
+  (void)L;
+}
+
+// z_k = RN(y_k + RN(+-alpha x_k))
+template <int K>
+__global__ void __launch_bounds__(32 * KW) waxpy(int64_t n, VecIn alpha, int negate, VecIn x, VecIn y,
+                                                 YView z, const int* stop) {
+  constexpr int L = 32 * K;
+  if (stop && *stop) return;
+  extern __shared__ uint32_t wsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* sA = wsm + warp * 8 * L;
+  WMP<K> al;
+  wload<K>(alpha, 0, lane, al);
+  for (int64_t k = (int64_t)blockIdx.x * KW + warp; k < n; k += (int64_t)gridDim.x * KW) {
+    WMP<K> xv, s, t;
+    wload<K>(x, k, lane, xv);
+    wload<K>(y, k, lane, s);
+    wmul<K>(al.m, al.e, al.s ^ (uint32_t)negate, xv.m, xv.e, xv.s, sA, sA + L, sA + 2 * L, lane, t);
+    wadd<K>(s, t, sA + 2 * L, lane);
+    wstore<K>(z, k, lane, s);
+    __syncwarp();
+  }
+}
+
+enum { S_RHO = KS_RHO, S_RHOP = KS_RHOP, S_SIGMA = KS_SIGMA, S_ALPHA = KS_ALPHA, S_BETA = KS_BETA,
+       S_RR = KS_RR, S_NRM = KS_NRM, S_THR = KS_THR, S_C1 = KS_C1, S_C2 = KS_C2, S_ONE = KS_ONE,
+       S_T20 = KS_T20, S_T50 = KS_T50, S_ALPHAP = KS_ALPHAP, S_ZETA = KS_ZETA, S_ETA = KS_ETA,
+       S_MU1 = KS_MU1, S_MU2 = KS_MU2, S_MU3 = KS_MU3, S_MU4 = KS_MU4, S_MU5 = KS_MU5,
+       S_TAU = KS_TAU };
+enum { F_STOP = KF_STOP, F_BREAK = KF_BREAK, F_CONV = KF_CONV, F_BRK2 = KF_BRK2 };
+
+// the scalar steps of krylov.cu bicg_scalar (same op numbers), one warp
+template <int K>
+__global__ void __launch_bounds__(32) wscalar(YView S, int* fl, int op) {
+  constexpr int L = 32 * K;
+  if (fl[F_STOP]) return;
+  extern __shared__ uint32_t wsm[];
+  const int lane = threadIdx.x & 31;
+  uint32_t* sA = wsm;
+  uint32_t* sX = wsm + L;
+  uint32_t* cs = wsm + 2 * L;                        // 6L words: wmul / wadd / big-int scratch
+  const VecIn Sv{S.limbs, S.exps, S.signs};
+  auto ld = [&](int i, WMP<K>& a) { wload<K>(Sv, i, lane, a); };
+  auto st = [&](int i, const WMP<K>& a) { wstore<K>(S, i, lane, a); __syncwarp(); };
+  auto mul = [&](const WMP<K>& a, const WMP<K>& b, WMP<K>& o) {
+    wmul<K>(a.m, a.e, a.s, b.m, b.e, b.s, sA, sX, cs, lane, o);
+    __syncwarp();
+  };
+  auto add = [&](WMP<K>& s, const WMP<K>& t) { wadd<K>(s, t, cs, lane); __syncwarp(); };
+  auto det = [&](const WMP<K>& a, const WMP<K>& b, const WMP<K>& c, const WMP<K>& d, WMP<K>& o) {
+    WMP<K> t;
+    mul(a, b, o);
+    mul(c, d, t);
+    t.s ^= 1u;
+    add(o, t);
+  };
+  auto div = [&](const WMP<K>& a, const WMP<K>& b, WMP<K>& o) { wdiv<K>(a, b, o, cs, lane); __syncwarp(); };
+  auto sqr = [&](const WMP<K>& a, WMP<K>& o) { wsqrt<K>(a, o, cs, lane); __syncwarp(); };
+  auto flag = [&](int f) { if (lane == 0) fl[f] = 1; };
+  WMP<K> a, b, c;
+  switch (op) {
+    case 0: {
+      WMP<K> c1, t;
+      ld(S_ONE, a);
+      ld(S_T20, b);
+      div(a, b, c1);
+      st(S_C1, c1);
+      ld(S_T50, b);
+      div(a, b, c);
+      st(S_C2, c);
+      ld(S_RR, a);
+      sqr(a, b);                                     // nrm0
+      mul(c1, b, t);
+      add(t, c);
+      st(S_THR, t);
+      break;
+    }
+    case 1:
+      ld(S_RHO, a);
+      if (wzero<K>(a)) { flag(F_BREAK); flag(F_STOP); }
+      break;
+    case 2:
+      ld(S_RHO, a);
+      ld(S_RHOP, b);
+      div(a, b, c);
+      st(S_BETA, c);
+      break;
+    case 3:
+      ld(S_RHO, a);
+      ld(S_SIGMA, b);
+      if (wzero<K>(b)) { flag(F_BREAK); flag(F_STOP); break; }
+      div(a, b, c);
+      st(S_ALPHA, c);
+      break;
+    case 4:
+      ld(S_RR, a);
+      sqr(a, b);
+      st(S_NRM, b);
+      ld(S_THR, c);
+      if (wcmp<K>(b, c) <= 0) { flag(F_CONV); flag(F_STOP); }
+      ld(S_RHO, a);
+      st(S_RHOP, a);
+      break;
+    case 5:
+      ld(S_MU2, a);
+      ld(S_MU5, b);
+      if (wzero<K>(b)) wset_zero<K>(c); else div(a, b, c);
+      st(S_ZETA, c);
+      wset_zero<K>(c);
+      st(S_ETA, c);
+      break;
+    case 6: {
+      WMP<K> d, e;
+      ld(S_RHO, a);
+      ld(S_RHOP, b);
+      div(a, b, c);
+      ld(S_ALPHAP, a);
+      ld(S_ZETA, b);
+      div(a, b, d);
+      mul(c, d, e);
+      st(S_BETA, e);
+      break;
+    }
+    case 7: {
+      WMP<K> m1, m2, m3, m4, m5, tau, num;
+      ld(S_MU1, m1);
+      ld(S_MU2, m2);
+      ld(S_MU3, m3);
+      ld(S_MU4, m4);
+      ld(S_MU5, m5);
+      det(m5, m1, m4, m4, tau);
+      st(S_TAU, tau);
+      if (wzero<K>(tau)) { flag(F_BREAK); flag(F_STOP); break; }
+      det(m1, m2, m3, m4, num);
+      div(num, tau, c);
+      st(S_ZETA, c);
+      det(m5, m3, m4, m2, num);
+      div(num, tau, c);
+      st(S_ETA, c);
+      break;
+    }
+    case 8:
+      ld(S_RR, a);
+      sqr(a, b);
+      st(S_NRM, b);
+      ld(S_THR, c);
+      if (wcmp<K>(b, c) <= 0) {
+        flag(F_CONV); flag(F_STOP);
+      } else {
+        ld(S_ZETA, a);
+        if (wzero<K>(a)) { flag(F_BRK2); flag(F_STOP); }
+      }
+      ld(S_RHO, a);
+      st(S_RHOP, a);
+      ld(S_ALPHA, a);
+      st(S_ALPHAP, a);
+      break;
+  }
+}
+
+template <int K>
+struct WideOps {
+  static constexpr int L = 32 * K;
+  static constexpr size_t SM = (size_t)8 * L * 4;   // per-warp shared memory (bytes)
+  template <class Kern>
+  static int attr(Kern k, size_t bytes) {
+    return (int)cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  }
+  static size_t bytes(int64_t n) {
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    return al((size_t)n * L * 4) + al((size_t)n * 4) + al((size_t)n);
+  }
+  static int dot(int64_t n, VecIn u, VecIn v, YView out, const int* stop, cudaStream_t st, void* work) {
+    if (!work && n > 0) return (int)cudaErrorInvalidValue;
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    char* p = (char*)work;
+    YView P{(uint32_t*)p, (int32_t*)(p + al((size_t)n * L * 4)),
+            (uint8_t*)(p + al((size_t)n * L * 4) + al((size_t)n * 4))};
+    int e;
+    if (n > 0) {
+      if ((e = attr(wdot_products<K>, KW * SM))) return e;
+      const int64_t blocks = std::min<int64_t>((n + KW - 1) / KW, 148 * 16);
+      wdot_products<K><<<(unsigned)blocks, 32 * KW, KW * SM, st>>>(n, u, v, P, stop);
+      launch_counter_add(1);
+    }
+    if ((e = attr(wdot_chain<K>, SM))) return e;
+    wdot_chain<K><<<1, 32, SM, st>>>(n, VecIn{P.limbs, P.exps, P.signs}, out, stop);
+    launch_counter_add(1);
+    return (int)cudaGetLastError();
+  }
+  static int axpy(int64_t n, VecIn a, int neg, VecIn x, VecIn y, YView z, const int* stop, cudaStream_t st) {
+    if (n <= 0) return 0;
+    int e;
+    if ((e = attr(waxpy<K>, KW * SM))) return e;
+    const int64_t blocks = std::min<int64_t>((n + KW - 1) / KW, 148 * 16);
+    waxpy<K><<<(unsigned)blocks, 32 * KW, KW * SM, st>>>(n, a, neg, x, y, z, stop);
+    launch_counter_add(1);
+    return (int)cudaGetLastError();
+  }
+  static int scalar(YView S, int* fl, int op, cudaStream_t st) {
+    int e;
+    if ((e = attr(wscalar<K>, SM))) return e;
+    wscalar<K><<<1, 32, SM, st>>>(S, fl, op);
+    launch_counter_add(1);
+    return (int)cudaGetLastError();
+  }
+};
+
+}  // namespace wide
+
+int krylov_wide_dot(int L, int64_t n, const VecIn& u, const VecIn& v, const YView& out, const int* stop,
+                    void* stream, void* work) {
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (L) {
+    case 64: return wide::WideOps<2>::dot(n, u, v, out, stop, st, work);
+    case 128: return wide::WideOps<4>::dot(n, u, v, out, stop, st, work);
+    case 256: return wide::WideOps<8>::dot(n, u, v, out, stop, st, work);
+    default: return (int)cudaErrorInvalidValue;
+  }
+}
+
+size_t krylov_wide_dot_work_bytes(int L, int64_t n) {
+  switch (L) {
+    case 64: return wide::WideOps<2>::bytes(n);
+    case 128: return wide::WideOps<4>::bytes(n);
+    case 256: return wide::WideOps<8>::bytes(n);
+    default: return 0;
+  }
+}
+
+int krylov_wide_axpy(int L, int64_t n, const VecIn& al, int neg, const VecIn& x, const VecIn& y,
+                     const YView& z, const int* stop, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (L) {
+    case 64: return wide::WideOps<2>::axpy(n, al, neg, x, y, z, stop, st);
+    case 128: return wide::WideOps<4>::axpy(n, al, neg, x, y, z, stop, st);
+    case 256: return wide::WideOps<8>::axpy(n, al, neg, x, y, z, stop, st);
+    default: return (int)cudaErrorInvalidValue;
+  }
+}
+
+int krylov_wide_scalar(int L, const YView& S, int* fl, int op, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (L) {
+    case 64: return wide::WideOps<2>::scalar(S, fl, op, st);
+    case 128: return wide::WideOps<4>::scalar(S, fl, op, st);
+    case 256: return wide::WideOps<8>::scalar(S, fl, op, st);
+    default: return (int)cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace mpsp

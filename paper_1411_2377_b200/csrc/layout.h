@@ -97,6 +97,13 @@ int krylov_dot_stats(unsigned long long out[2]);   // [sequential, validated] se
 int krylov_axpy(int L, int64_t n, const VecIn& al, int neg, const VecIn& x, const VecIn& y,
                 const YView& z, const int* stop, void* stream);
 int krylov_scalar(int L, const YView& S, int* fl, int op, void* stream);
+// the same at L = 64, 128, 256 (krylov_wide.cu; the dot always needs `work`)
+int krylov_wide_dot(int L, int64_t n, const VecIn& u, const VecIn& v, const YView& out,
+                    const int* stop, void* stream, void* work);
+size_t krylov_wide_dot_work_bytes(int L, int64_t n);
+int krylov_wide_axpy(int L, int64_t n, const VecIn& al, int neg, const VecIn& x, const VecIn& y,
+                     const YView& z, const int* stop, void* stream);
+int krylov_wide_scalar(int L, const YView& S, int* fl, int op, void* stream);
 enum { KS_RHO, KS_RHOP, KS_SIGMA, KS_ALPHA, KS_BETA, KS_RR, KS_NRM, KS_THR, KS_C1, KS_C2, KS_ONE,
        KS_T20, KS_T50, KS_ALPHAP, KS_ZETA, KS_ETA, KS_MU1, KS_MU2, KS_MU3, KS_MU4, KS_MU5, KS_TAU,
        KS_N };

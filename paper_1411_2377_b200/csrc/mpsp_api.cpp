@@ -659,7 +659,6 @@ namespace {
 
 int check_vec_args(int p_bits, int64_t n, const void* a, const void* b, const void* c) {
   if (!mpsp_supported_precision(p_bits) || n < 0) return n < 0 ? MPSP_E_ARG : MPSP_E_PREC;
-  if (p_bits > 1024) return MPSP_E_PREC;              // vector kernels: L <= 32
   if (n > 0 && (!a || !b || !c)) return MPSP_E_ARG;
   return MPSP_OK;
 }
@@ -715,7 +714,7 @@ int mpsp_dot(int p_bits, int64_t n, const uint32_t* u_limbs, const int32_t* u_ex
   cudaStream_t st = (cudaStream_t)cuda_stream;
   void* work = nullptr;
   const char* ns = std::getenv("MPSP_DOT_ONEWARP");           // debug: plain one-warp chain
-  const size_t wb = (ns && ns[0] == '1') ? 0 : krylov_dot_work_bytes(L, n);
+  const size_t wb = (ns && ns[0] == '1' && L <= 32) ? 0 : krylov_dot_work_bytes(L, n);
   if (wb && cudaMallocAsync(&work, wb, st) != cudaSuccess) { cudaGetLastError(); return MPSP_E_NOMEM; }
   const int e = krylov_dot(L, n, u, v, o, nullptr, cuda_stream, work);
   if (work) cudaFreeAsync(work, st);
@@ -743,7 +742,7 @@ int mpsp_bicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, const
   if (!A || !iters || !status || max_iter < 0) return MPSP_E_ARG;
   if (!A->has_t) return MPSP_E_NOTRANS;
   if (A->rb != 0 || A->re != A->n) return MPSP_E_ARG;   // needs the whole matrix
-  if (A->p < 128 || A->L > 32) return MPSP_E_PREC;       // 10^50 exact in p bits; no wide solver yet
+  if (A->p < 128) return MPSP_E_PREC;                     // 10^50 exact in p bits
   const int L = A->L;
   const int64_t n = A->n;
   *iters = 0;
@@ -852,7 +851,7 @@ int mpsp_gpbicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, con
                 int* status, void* cuda_stream) {
   if (!A || !iters || !status || max_iter < 0) return MPSP_E_ARG;
   if (A->rb != 0 || A->re != A->n) return MPSP_E_ARG;   // needs the whole matrix
-  if (A->p < 128 || A->L > 32) return MPSP_E_PREC;
+  if (A->p < 128) return MPSP_E_PREC;
   const int L = A->L;
   const int64_t n = A->n;
   *iters = 0;

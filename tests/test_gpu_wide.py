@@ -47,18 +47,11 @@ def test_wide_config_shapes(cfg, n, p):
         assert_same(gpu_run(d, op), oracle_full(d, op), f"{cfg} n={n} p={p} {op}")
 
 
-def test_wide_row_block_and_solver_rejection():
-    """A row block at p = 2048 equals the same rows of the full result; the
-    solvers (and the vector kernels) stay limited to p <= 1024."""
-    from paper_1411_2377_b200 import CSR, MPVec, MpspError
+def test_wide_row_block():
+    """A row block at p = 2048 equals the same rows of the full result."""
     d = gen.stress(2048, seed=2, long_len=200)
     full = oracle_full(d, "ax")
     n = d["n"]
     rb, re = n // 3, n // 3 + 101
     got = gpu_run(d, "ax", rows=(rb, re))
     assert_same(got, tuple(a[rb:re] for a in full), "row block")
-    A = CSR(d["p"], d["rowptr"], d["colidx"], d["limbs"], d["exps"], d["signs"], transpose=True)
-    b = MPVec.from_host(d["x_limbs"], d["x_exps"], d["x_signs"], device="cuda:0")
-    with pytest.raises(MpspError):
-        A.bicg(b, 3)
-    A.close()
