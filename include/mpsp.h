@@ -68,10 +68,10 @@ typedef struct mpsp_csr mpsp_csr;
  *
  *   out        receives the handle (NULL on error; nothing leaks on error).
  *   p_bits     precision p in bits; supported: 32, 64, 128, 256, 512, 1024
- *              (L = p/32 in {1,2,4,8,16,32}) and, for SpMV only, the
- *              paper's solver precisions 2048, 4096, 8192 (L = 64, 128,
- *              256; one warp per row with the
- *              limbs spread across the lanes).
+ *              (L = p/32 in {1,2,4,8,16,32}) and the paper's solver
+ *              precisions 2048, 4096, 8192 (L = 64, 128, 256;
+ *              one warp per row with the limbs
+ *              spread across the lanes).
  *   n          A is n x n (n >= 0).
  *   rowptr     host int64[n+1]: CSR row pointers (rowptr[0] = 0, monotone).
  *   colidx     host int32[nnz], nnz = rowptr[n] <= 2^31-1; strictly
@@ -201,8 +201,9 @@ int64_t mpsp_launch_count(void);
 #define MPSP_BICG_BREAKDOWN  1   /* rho = 0 or (p~, z) = 0 */
 #define MPSP_BICG_MAXITER    2
 
-/* The vector and solver calls below support 32 <= p <= 1024 (mpsp_bicg /
- * mpsp_gpbicg: 128 <= p <= 1024); other p -> MPSP_E_PREC. */
+/* The vector and solver calls below support every precision mpsp_csr_create
+ * does (mpsp_bicg / mpsp_gpbicg: p >= 128); at p > 1024 they run on
+ * warp-distributed values (krylov_wide.cu); other p -> MPSP_E_PREC. */
 
 /* out = (u, v): ordered rounded chain over k = 0..n-1 (one element, device). */
 int mpsp_dot(int p_bits, int64_t n,
