@@ -3,8 +3,9 @@
 // and more), on warp-distributed values
 // (wide_mp.cuh).  Same operations and readings as krylov.cu:
 //   dot   : s = RN(s + RN(u_k v_k)), k ascending, from +0.  Products in
-//           parallel (a warp per element), then ONE warp walks the ordered
-//           chain of adds (a sequential chain; no speculation at these L yet).
+//           parallel (a warp per element); the ordered chain of adds split
+//           into segments evaluated speculatively in parallel and validated
+//           in order by one warp (see wseg_*).
 //   axpy  : z_k = RN(y_k + RN(+-alpha x_k)), a warp per element.
 //   scalar: the solver's scalar steps (krylov.cu bicg_scalar ops 0-8) in one
 //           warp: RN division by restoring long division (p+4 quotient bits,
@@ -285,7 +286,7 @@ constexpr int KW = 4;                                // warps per block
 // t_k = RN(u_k v_k) into the scratch vector P (ABI element layout)
 template <int K>
 __global__ void __launch_bounds__(32 * KW) wdot_products(int64_t n, VecIn u, VecIn v, YView P,
-                                                         const int* stop) {
+                                                         double* fp, const int* stop) {
   constexpr int L = 32 * K;
   if (stop && *stop) return;
   extern __shared__ uint32_t wsm[];
@@ -297,28 +298,221 @@ __global__ void __launch_bounds__(32 * KW) wdot_products(int64_t n, VecIn u, Vec
     wload<K>(v, k, lane, b);
     wmul<K>(a.m, a.e, a.s, b.m, b.e, b.s, sA, sA + L, sA + 2 * L, lane, t);
     wstore<K>(P, k, lane, t);
+    if (fp && lane == 31) {                        // fp64 estimate from the top two limbs
+      const unsigned long long top = ((unsigned long long)t.m[K - 1] << 32) | t.m[K - 2];
+      const double dv = t.m[K - 1] ? ldexp(__ull2double_rn(top), t.e - 64) : 0.0;
+      fp[k] = t.s ? -dv : dv;
+    }
     __syncwarp();
   }
 }
 
-// out = the ordered chain of adds over P[0..n)
+// ------------------------------------------- segmented speculative dot chain
+// (krylov.cu's segmented dot, on warp-distributed values)
+//  S1: the products t_k and fp64 estimates (wdot_products);
+//  S2: fp64 sum per segment of WSEG products;
+//  S3 (a warp per segment s >= 1): the accumulator's binade E_g and sign at
+//      the segment start GUESSED from the fp64 prefix; each step's grid
+//      increment Q_k = +-RN_int(|t_k| / 2^(E_g - p)) is added EXACTLY to a
+//      two's complement big integer R (W words per lane), the minimum and
+//      maximum of the partial sums R_k recorded; a tie on the grid or a
+//      product reaching the binade (t.e >= E_g) invalidates the segment;
+//  S4 (one warp): the chain walks the segments in order; when the exact state
+//      s = S 2^(E - p) has E = E_g, the guessed sign, and S + min >= 2^(p-1)+1,
+//      S + max <= 2^p - 1, every step of the segment is S += Q_k on the grid
+//      (RN(S u + t_k) = (S + Q_k) u: no tie, no binade change), so S += R;
+//      any other segment is walked step by step with wadd from the stored
+//      products.  The result is the ordered chain's, bit for bit.
+constexpr int WSEG = 64;
+
 template <int K>
-__global__ void __launch_bounds__(32) wdot_chain(int64_t n, VecIn P, YView out, const int* stop) {
-  constexpr int L = 32 * K;
+struct WSeg {
+  static constexpr int W = K + 1;                  // big-integer words per lane
+  double* fp;          // [n]
+  double* segsum;      // [nseg]
+  int32_t* valid;      // [nseg]
+  int32_t* eg;         // [nseg]
+  uint32_t* sg;        // [nseg]
+  uint32_t* ds;        // [nseg][32 W]
+  uint32_t* mn;        // [nseg][32 W]
+  uint32_t* mx;        // [nseg][32 W]
+};
+
+template <int K>
+__global__ void __launch_bounds__(128) wseg_sums(int64_t n, int64_t nseg, WSeg<K> G, const int* stop) {
+  if (stop && *stop) return;
+  const int64_t seg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (seg >= nseg) return;
+  double acc = 0.0;
+  for (int j = lane; j < WSEG; j += 32) {
+    const int64_t k = seg * WSEG + j;
+    if (k < n) acc += G.fp[k];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+  if (lane == 0) G.segsum[seg] = acc;
+}
+
+// signed a < b for two's complement big integers
+template <int W>
+__device__ __forceinline__ bool wi_slt(const uint32_t (&a)[W], const uint32_t (&b)[W], int lane) {
+  uint32_t x[W], y[W];
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    const uint32_t f = (lane == 31 && i == W - 1) ? 0x80000000u : 0u;
+    x[i] = a[i] ^ f;
+    y[i] = b[i] ^ f;
+  }
+  return wi_lt<W>(x, y);
+}
+
+template <int W>
+__device__ __forceinline__ void wi_load(const uint32_t* g, uint32_t (&a)[W], int lane) {
+#pragma unroll
+  for (int i = 0; i < W; ++i) a[i] = g[lane * W + i];
+}
+template <int W>
+__device__ __forceinline__ void wi_store(uint32_t* g, const uint32_t (&a)[W], int lane) {
+#pragma unroll
+  for (int i = 0; i < W; ++i) g[lane * W + i] = a[i];
+}
+
+template <int K>
+__global__ void __launch_bounds__(32 * KW) wseg_speculate(int64_t n, int64_t nseg, VecIn P, WSeg<K> G,
+                                                          const int* stop) {
+  constexpr int L = 32 * K, W = K + 1, PB = 32 * L;
+  if (stop && *stop) return;
+  extern __shared__ uint32_t wsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t seg = (int64_t)blockIdx.x * KW + warp;
+  if (seg >= nseg || seg == 0) return;
+  uint32_t* sm = wsm + warp * 8 * L;               // 2L + 34 words used
+  double pre = 0.0;
+  for (int64_t j = lane; j < seg; j += 32) pre += G.segsum[j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(FULL, pre, o);
+  int e2 = 0;
+  frexp(fabs(pre), &e2);
+  bool valid = pre != 0.0 && isfinite(pre);
+  const int32_t Eg = e2;
+  const uint32_t sgg = pre < 0.0 ? 1u : 0u;
+  uint32_t R[W], mn[W], mx[W];
+#pragma unroll
+  for (int i = 0; i < W; ++i) { R[i] = 0u; mn[i] = 0u; mx[i] = 0u; }
+  for (int j = 0; j < WSEG && valid; ++j) {
+    const int64_t k = seg * WSEG + j;
+    if (k >= n) break;
+    WMP<K> t;
+    wload<K>(P, k, lane, t);
+    if (wzero<K>(t)) continue;
+    const int64_t d = (int64_t)Eg - (int64_t)t.e;   // |t| / u = M_t / 2^d
+    if (d < 1) { valid = false; break; }            // reaches the binade
+    if (d > PB + 2) continue;                       // |t| < u/4: Q = 0
+    // Y = floor(M_t / 2^d), rb = bit d-1, sticky = bits below it
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < K; ++i) { sm[lane * K + i] = t.m[i]; sm[L + 1 + lane * K + i] = 0u; }
+    if (lane == 0) { sm[L] = 0u; sm[2 * L + 1] = 0u; sm[2 * L + 2] = 0u; }
+    __syncwarp();
+    const int q = (int)(d >> 5);
+    const uint32_t r = (uint32_t)d & 31u;
+    uint32_t Q[W];
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      const int m = lane * W + i + q;               // source word of Y word lane*W+i
+      const uint32_t lo_ = m <= 2 * L + 1 ? sm[m] : 0u;
+      const uint32_t hi_ = m + 1 <= 2 * L + 1 ? sm[m + 1] : 0u;
+      Q[i] = (m < 2 * L + 2) ? __funnelshift_r(lo_, hi_, r) : 0u;
+    }
+    const int64_t rp = d - 1;                       // round bit position in M_t
+    const uint32_t rb = (sm[rp >> 5] >> (rp & 31)) & 1u;
+    uint32_t orr = 0u;
+    for (int w = lane; w < (int)(rp >> 5); w += 32) orr |= sm[w];
+    if (lane == 0) orr |= sm[rp >> 5] & ((1u << (rp & 31)) - 1u);
+    const bool sticky = __ballot_sync(FULL, orr != 0u) != 0u;
+    __syncwarp();
+    if (rb && !sticky) { valid = false; break; }    // grid tie: needs the parity of S
+    if (rb) {
+      uint32_t one[W];
+#pragma unroll
+      for (int i = 0; i < W; ++i) one[i] = (lane == 0 && i == 0) ? 1u : 0u;
+      wi_add<W>(Q, one, lane);
+    }
+    if (t.s == sgg) wi_add<W>(R, Q, lane); else wi_sub<W>(R, Q, lane);
+    if (wi_slt<W>(R, mn, lane)) {
+#pragma unroll
+      for (int i = 0; i < W; ++i) mn[i] = R[i];
+    }
+    if (wi_slt<W>(mx, R, lane)) {
+#pragma unroll
+      for (int i = 0; i < W; ++i) mx[i] = R[i];
+    }
+  }
+  if (lane == 0) {
+    G.valid[seg] = valid ? 1 : 0;
+    G.eg[seg] = Eg;
+    G.sg[seg] = sgg;
+  }
+  wi_store<W>(G.ds + seg * 32 * W, R, lane);
+  wi_store<W>(G.mn + seg * 32 * W, mn, lane);
+  wi_store<W>(G.mx + seg * 32 * W, mx, lane);
+}
+
+template <int K>
+__global__ void __launch_bounds__(32) wseg_chain(int64_t n, int64_t nseg, VecIn P, WSeg<K> G,
+                                                 YView out, const int* stop) {
+  constexpr int L = 32 * K, W = K + 1;
   if (stop && *stop) return;
   extern __shared__ uint32_t wsm[];
   const int lane = threadIdx.x & 31;
-  WMP<K> s, t, nx;
+  uint32_t LO[W], HI[W];                            // 2^(p-1) + 1, 2^p - 1
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    const int w = lane * W + i;
+    LO[i] = w == 0 ? 1u : (w == L - 1 ? 0x80000000u : 0u);
+    HI[i] = w < L ? 0xffffffffu : 0u;
+  }
+  WMP<K> s;
   wset_zero<K>(s);
-  if (n > 0) wload<K>(P, 0, lane, nx);
-  for (int64_t k = 0; k < n; ++k) {
-    t = nx;
-    if (k + 1 < n) wload<K>(P, k + 1, lane, nx);
-    wadd<K>(s, t, wsm, lane);
-    __syncwarp();
+  for (int64_t seg = 0; seg < nseg; ++seg) {
+    bool ok = seg > 0 && G.valid[seg] && !wzero<K>(s) && G.eg[seg] == s.e && G.sg[seg] == s.s;
+    uint32_t S[W];
+    if (ok) {
+      to_wi<K, W>(s.m, S, wsm, lane);
+      uint32_t A[W], B[W], M[W];
+      wi_load<W>(G.mn + seg * 32 * W, M, lane);
+#pragma unroll
+      for (int i = 0; i < W; ++i) A[i] = S[i];
+      wi_add<W>(A, M, lane);
+      wi_load<W>(G.mx + seg * 32 * W, M, lane);
+#pragma unroll
+      for (int i = 0; i < W; ++i) B[i] = S[i];
+      wi_add<W>(B, M, lane);
+      ok = !wi_slt<W>(A, LO, lane) && !wi_slt<W>(HI, B, lane);
+    }
+    if (ok) {
+      uint32_t D[W];
+      wi_load<W>(G.ds + seg * 32 * W, D, lane);
+      wi_add<W>(S, D, lane);
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < W; ++i) wsm[lane * W + i] = S[i];
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < K; ++i) s.m[i] = wsm[lane * K + i];
+      __syncwarp();
+    } else {
+      const int64_t k1 = min(n, (seg + 1) * WSEG);
+      WMP<K> t;
+      for (int64_t k = seg * WSEG; k < k1; ++k) {
+        wload<K>(P, k, lane, t);
+        wadd<K>(s, t, wsm, lane);
+        __syncwarp();
+      }
+    }
   }
   wstore<K>(out, 0, lane, s);
-  (void)L;
 }
 
 // z_k = RN(y_k + RN(+-alpha x_k))
@@ -489,23 +683,42 @@ struct WideOps {
   }
   static size_t bytes(int64_t n) {
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-    return al((size_t)n * L * 4) + al((size_t)n * 4) + al((size_t)n);
+    const size_t nseg = (size_t)((n + WSEG - 1) / WSEG);
+    constexpr int W = K + 1;
+    return al((size_t)n * L * 4) + al((size_t)n * 4) + al((size_t)n) + al((size_t)n * 8) +
+           al(nseg * 8) + 3 * al(nseg * 4) + 3 * al(nseg * 32 * W * 4);
   }
   static int dot(int64_t n, VecIn u, VecIn v, YView out, const int* stop, cudaStream_t st, void* work) {
     if (!work && n > 0) return (int)cudaErrorInvalidValue;
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    constexpr int W = K + 1;
+    const int64_t nseg = (n + WSEG - 1) / WSEG;
     char* p = (char*)work;
     YView P{(uint32_t*)p, (int32_t*)(p + al((size_t)n * L * 4)),
             (uint8_t*)(p + al((size_t)n * L * 4) + al((size_t)n * 4))};
+    p += al((size_t)n * L * 4) + al((size_t)n * 4) + al((size_t)n);
+    WSeg<K> G;
+    G.fp = (double*)p; p += al((size_t)n * 8);
+    G.segsum = (double*)p; p += al((size_t)nseg * 8);
+    G.valid = (int32_t*)p; p += al((size_t)nseg * 4);
+    G.eg = (int32_t*)p; p += al((size_t)nseg * 4);
+    G.sg = (uint32_t*)p; p += al((size_t)nseg * 4);
+    G.ds = (uint32_t*)p; p += al((size_t)nseg * 32 * W * 4);
+    G.mn = (uint32_t*)p; p += al((size_t)nseg * 32 * W * 4);
+    G.mx = (uint32_t*)p;
+    const VecIn Pin{P.limbs, P.exps, P.signs};
     int e;
     if (n > 0) {
       if ((e = attr(wdot_products<K>, KW * SM))) return e;
       const int64_t blocks = std::min<int64_t>((n + KW - 1) / KW, 148 * 16);
-      wdot_products<K><<<(unsigned)blocks, 32 * KW, KW * SM, st>>>(n, u, v, P, stop);
-      launch_counter_add(1);
+      wdot_products<K><<<(unsigned)blocks, 32 * KW, KW * SM, st>>>(n, u, v, P, G.fp, stop);
+      wseg_sums<K><<<(unsigned)((nseg * 32 + 127) / 128), 128, 0, st>>>(n, nseg, G, stop);
+      if ((e = attr(wseg_speculate<K>, KW * SM))) return e;
+      wseg_speculate<K><<<(unsigned)((nseg + KW - 1) / KW), 32 * KW, KW * SM, st>>>(n, nseg, Pin, G, stop);
+      launch_counter_add(3);
     }
-    if ((e = attr(wdot_chain<K>, SM))) return e;
-    wdot_chain<K><<<1, 32, SM, st>>>(n, VecIn{P.limbs, P.exps, P.signs}, out, stop);
+    if ((e = attr(wseg_chain<K>, SM))) return e;
+    wseg_chain<K><<<1, 32, SM, st>>>(n, nseg, Pin, G, out, stop);
     launch_counter_add(1);
     return (int)cudaGetLastError();
   }

@@ -111,3 +111,20 @@ def test_wide_bicg_identity_converges():
     assert (it, status) == (1, "converged")
     assert_same(x.to_host(), oracle.pack_vec(b, p), "identity")
     H.close()
+
+
+@pytest.mark.parametrize("kind", ["random", "positive", "growing", "cancel", "huge", "ties"])
+def test_wide_dot_segmented_paths(kind):
+    """The segmented speculative dot at p = 2048 (64-element segments) must
+    equal the ordered chain in every regime: committed segments, drifting
+    binade, exact cancellation to +0, fp64-overflowing guesses, grid ties."""
+    import zlib
+    import torch
+    from paper_1411_2377_b200.csr import dot
+    from test_gpu_krylov import _dot_case
+    p, n = 2048, 3000
+    rng = np.random.default_rng(zlib.crc32(f"wide-{kind}".encode()))
+    u, v = _dot_case(kind, n, p, rng)
+    got = dot(p, _vec(u, p), _vec(v, p))
+    torch.cuda.synchronize()
+    assert_same(got.to_host(), oracle.pack_vec([K.dot(u, v, p)], p), f"dot {kind}")
