@@ -68,6 +68,8 @@ from paper_1411_2377_b200 import _lib  # noqa: E402
 st = (ctypes.c_ulonglong * 2)()
 _lib.lib().mpsp_debug_dot_stats(st)
 print("dot segments over the run: sequential", st[0], "validated", st[1])
+A.gpbicg(b, 2)                              # warm-up (kernel loading, clocks)
+torch.cuda.synchronize()
 e0.record()
 xg, itg, statusg = A.gpbicg(b, iters)
 e1.record()
