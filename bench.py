@@ -370,8 +370,9 @@ def main():
     # the algorithmic count is the schoolbook L^2 per nnz; the
     # short product with its exactness certificate executes fewer (DESIGN.md
     # "Product"), so frac can exceed 1: also report the IMAD pipe's own load
-    # (p > 1024, spmv_wide: the full product plus the diagonal chunks' second MAC)
-    ex_per = (L * L - (L - 3) * (L - 2) // 2 if L >= 4 else L * L) if L <= 32 else L * L + 32 * L
+    # (p > 1024, spmv_wide's short product: the hi columns, diagonal chunks
+    # included, plus the three top lo columns: L^2/2 + 19L)
+    ex_per = (L * L - (L - 3) * (L - 2) // 2 if L >= 4 else L * L) if L <= 32 else L * L // 2 + 19 * L
     roof["executed_macs_per_nnz"] = ex_per
     roof["frac_executed"] = (nnz_local * ex_per / kern_avg_s) / int_peak
 

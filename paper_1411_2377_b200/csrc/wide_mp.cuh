@@ -83,26 +83,18 @@ __device__ __forceinline__ uint32_t wround(uint32_t (&m)[K], uint32_t inc, int l
   return cout;
 }
 
-// t = RN(a * x).  sA, sX: L words each, cs: 6L words (per-warp shared memory).
-template <int K>
-__device__ __forceinline__ void wmul(const uint32_t (&a)[K], int32_t ea, uint32_t sa,
-                                     const uint32_t (&x)[K], int32_t ex, uint32_t sx,
-                                     uint32_t* sA, uint32_t* sX, uint32_t* cs, int lane,
-                                     WMP<K>& t) {
+// Comba column sums of a x (operands in sA, sX) into cs0/cs1/cs2 = cs,
+// cs + 2L, cs + 4L (three words per column, 2L columns).  Lane j owns columns
+// c = j + 32u and c + L (u < K): their term counts add up to L, so the MACs
+// are balanced; in the 32-step diagonal chunk (u == v) lanes switch from c to
+// c + L at different steps and both accumulators take a MAC (one with a zero
+// operand).  SHORT: only the columns >= L-3 (others written as 0): the hi
+// columns as above, the three top lo columns from per-lane partial sums over
+// i = j (mod 32) reduced across the warp - the lo MACs (u > v) are skipped.
+template <int K, bool SHORT>
+__device__ __forceinline__ void wcolumns(const uint32_t* sA, const uint32_t* sX, uint32_t* cs,
+                                         int lane) {
   constexpr int L = 32 * K;
-  const bool az = __shfl_sync(FULL, a[K - 1], 31) == 0u;
-  const bool xz = __shfl_sync(FULL, x[K - 1], 31) == 0u;
-  if (az || xz) {                                  // warp-uniform
-    wset_zero<K>(t);
-    return;
-  }
-#pragma unroll
-  for (int i = 0; i < K; ++i) {
-    sA[lane * K + i] = a[i];
-    sX[lane * K + i] = x[i];
-  }
-  __syncwarp();
-  // column sums: lo[u] = column lane + 32u, hi[u] = column lane + 32u + L
   uint64_t lo[K], hi[K];
   uint32_t lo2[K], hi2[K];
 #pragma unroll
@@ -117,15 +109,45 @@ __device__ __forceinline__ void wmul(const uint32_t (&a)[K], int32_t ea, uint32_
       for (int u = 0; u < K; ++u) {
         const int c = lane + 32 * u;
         if (u > v) {                               // i <= c: column c
-          mac64(lo[u], lo2[u], ai, sX[c - i]);
+          if (!SHORT) mac64(lo[u], lo2[u], ai, sX[c - i]);
         } else if (u < v) {                        // i > c: column c + L
           mac64(hi[u], hi2[u], ai, sX[c + L - i]);
-        } else {                                   // the diagonal chunk: both
+        } else if (SHORT) {                        // diagonal chunk, hi part only
+          const bool l = ii <= lane;
+          const uint32_t xv = sX[l ? 0 : c + L - i];
+          mac64(hi[u], hi2[u], ai, l ? 0u : xv);
+        } else {                                   // diagonal chunk: both
           const bool l = ii <= lane;
           const uint32_t xv = sX[l ? c - i : c + L - i];
           mac64(lo[u], lo2[u], ai, l ? xv : 0u);
           mac64(hi[u], hi2[u], ai, l ? 0u : xv);
         }
+      }
+    }
+  }
+  uint64_t top[3] = {0u, 0u, 0u};                  // SHORT: columns L-3, L-2, L-1
+  uint32_t top2[3] = {0u, 0u, 0u};
+  if (SHORT) {
+#pragma unroll
+    for (int m = 0; m < K; ++m) {
+      const int i = lane + 32 * m;
+      const uint32_t ai = sA[i];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const int xi = L - 3 + r - i;
+        const uint32_t xv = sX[xi >= 0 ? xi : 0];
+        mac64(top[r], top2[r], ai, xi >= 0 ? xv : 0u);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const uint64_t po = __shfl_xor_sync(FULL, top[r], o);
+        const uint32_t qo = __shfl_xor_sync(FULL, top2[r], o);
+        const uint64_t sum = top[r] + po;
+        top2[r] += qo + (sum < po ? 1u : 0u);
+        top[r] = sum;
       }
     }
   }
@@ -135,11 +157,31 @@ __device__ __forceinline__ void wmul(const uint32_t (&a)[K], int32_t ea, uint32_
 #pragma unroll
   for (int u = 0; u < K; ++u) {
     const int c = lane + 32 * u;
-    cs0[c] = (uint32_t)lo[u]; cs1[c] = (uint32_t)(lo[u] >> 32); cs2[c] = lo2[u];
+    uint64_t lv = lo[u];
+    uint32_t l2 = lo2[u];
+    if (SHORT) {
+      lv = 0u;
+      l2 = 0u;
+      if (u == K - 1 && lane >= 29) {
+        const int r = lane - 29;
+        lv = r == 0 ? top[0] : (r == 1 ? top[1] : top[2]);
+        l2 = r == 0 ? top2[0] : (r == 1 ? top2[1] : top2[2]);
+      }
+    }
+    cs0[c] = (uint32_t)lv; cs1[c] = (uint32_t)(lv >> 32); cs2[c] = l2;
     cs0[c + L] = (uint32_t)hi[u]; cs1[c + L] = (uint32_t)(hi[u] >> 32); cs2[c + L] = hi2[u];
   }
-  __syncwarp();
-  // limbs [2Kj, 2Kj + 2K) of the exact product P = sum_c col_c 2^(32c)
+}
+
+// The column sums in cs -> the product's limbs, written to cs[0 .. 2L) (lane
+// j sums limbs [2Kj, 2Kj+2K) lane-locally; the carry words are passed up one
+// lane and the one-bit ripple resolved by ripple()).
+template <int K>
+__device__ __forceinline__ void wcarry(uint32_t* cs, int lane) {
+  constexpr int L = 32 * K;
+  const uint32_t* cs0 = cs;
+  const uint32_t* cs1 = cs + 2 * L;
+  const uint32_t* cs2 = cs + 4 * L;
   uint32_t Pl[2 * K];
   uint64_t carry = 0u;
 #pragma unroll
@@ -163,27 +205,71 @@ __device__ __forceinline__ void wmul(const uint32_t (&a)[K], int32_t ea, uint32_
     inc_n<2 * K>(Pl, cin);
   }
   __syncwarp();                                    // everyone is done reading cs
-  uint32_t* Ps = cs;                               // P, 2L words
 #pragma unroll
-  for (int q = 0; q < 2 * K; ++q) Ps[2 * K * lane + q] = Pl[q];
+  for (int q = 0; q < 2 * K; ++q) cs[2 * K * lane + q] = Pl[q];
   __syncwarp();
-  const uint32_t sh = (~__shfl_sync(FULL, Pl[2 * K - 1], 31)) >> 31;   // top bit clear -> 1
+}
+
+// t = RN(a * x).  sA, sX: L words each, cs: 6L words (per-warp shared memory).
+// SHORT PRODUCT with an exactness certificate (the wide form of mp_mul's):
+// only the columns >= K0 = L-3 are formed; the omitted part is
+// N < K0 2^(32(L-2)) (1 + eps) < 2^B, B = 32(L-2) + 8 (K0 < 256), so if the
+// bits between B and the round bit are neither all 0 nor all 1, the rounded
+// product is the exact one's with sticky 1; otherwise (rare) the full product.
+template <int K>
+__device__ __forceinline__ void wmul(const uint32_t (&a)[K], int32_t ea, uint32_t sa,
+                                     const uint32_t (&x)[K], int32_t ex, uint32_t sx,
+                                     uint32_t* sA, uint32_t* sX, uint32_t* cs, int lane,
+                                     WMP<K>& t) {
+  constexpr int L = 32 * K;
+  const bool az = __shfl_sync(FULL, a[K - 1], 31) == 0u;
+  const bool xz = __shfl_sync(FULL, x[K - 1], 31) == 0u;
+  if (az || xz) {                                  // warp-uniform
+    wset_zero<K>(t);
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < K; ++i) {
-    const int m = lane * K + i;
-    t.m[i] = __funnelshift_l(Ps[L + m - 1], Ps[L + m], sh);
+    sA[lane * K + i] = a[i];
+    sX[lane * K + i] = x[i];
   }
-  const uint32_t wl = Ps[L - 1] << sh;             // the limb below the kept ones
-  uint32_t orr = 0u;
-  for (int k = lane; k < L - 1; k += 32) orr |= Ps[k];
-  const bool sticky = (__ballot_sync(FULL, orr != 0u) != 0u) || ((wl << 1) != 0u);
-  const uint32_t rb = wl >> 31;
-  const uint32_t lsb = __shfl_sync(FULL, t.m[0], 0) & 1u;
-  const uint32_t inc = rb & ((sticky ? 1u : 0u) | lsb);
-  __syncwarp();                                    // Ps reads done before cs is reused
-  const uint32_t cy = wround<K>(t.m, inc, lane);
-  if (cy && lane == 31) t.m[K - 1] = 0x80000000u;
-  t.e = ea + ex - (int32_t)sh + (int32_t)cy;
+  __syncwarp();
+  wcolumns<K, true>(sA, sX, cs, lane);
+  __syncwarp();
+  wcarry<K>(cs, lane);
+  const uint32_t* Ps = cs;                         // P (short: limbs >= L-3 valid), 2L words
+  uint32_t sh = (~Ps[2 * L - 1]) >> 31;            // top bit clear -> 1
+  {
+    const uint32_t wmask = (1u << (31u - sh)) - 1u;
+    const uint32_t w1 = Ps[L - 2] >> 8, w2 = Ps[L - 1] & wmask;
+    const bool amb = ((w1 | w2) == 0u) | ((w1 == 0x00FFFFFFu) & (w2 == wmask));
+    if (amb) {                                     // warp-uniform (same smem words): full product
+      __syncwarp();
+      wcolumns<K, false>(sA, sX, cs, lane);
+      __syncwarp();
+      wcarry<K>(cs, lane);
+      sh = (~Ps[2 * L - 1]) >> 31;
+    }
+    const uint32_t wl = Ps[L - 1] << sh;           // the limb below the kept ones
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const int m = lane * K + i;
+      t.m[i] = __funnelshift_l(Ps[L + m - 1], Ps[L + m], sh);
+    }
+    bool sticky = true;                            // certified: the window is nonzero
+    if (amb) {
+      uint32_t orr = 0u;
+      for (int k = lane; k < L - 1; k += 32) orr |= Ps[k];
+      sticky = (__ballot_sync(FULL, orr != 0u) != 0u) || ((wl << 1) != 0u);
+    }
+    const uint32_t rb = wl >> 31;
+    const uint32_t lsb = __shfl_sync(FULL, t.m[0], 0) & 1u;
+    const uint32_t inc = rb & ((sticky ? 1u : 0u) | lsb);
+    __syncwarp();                                  // Ps reads done before cs is reused
+    const uint32_t cy = wround<K>(t.m, inc, lane);
+    if (cy && lane == 31) t.m[K - 1] = 0x80000000u;
+    t.e = ea + ex - (int32_t)sh + (int32_t)cy;
+  }
   t.s = sa ^ sx;
 }
 
