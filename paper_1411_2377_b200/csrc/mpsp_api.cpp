@@ -865,12 +865,23 @@ int mpsp_gpbicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, con
   const size_t per = al(vl) + al(ve) + al(vs);
   const size_t sbytes = al((size_t)KS_N * L * 4) + al((size_t)KS_N * 4) + al(KS_N) + 256;
   const size_t dbytes = al(krylov_dot_work_bytes(L, n));
+  constexpr int ND = 5;         // the five independent inner products mu1..mu5 run concurrently
   char* ws = nullptr;
-  if ((ce = cudaMalloc(&ws, (NV + 2) * per + sbytes + dbytes)) != cudaSuccess) {
+  if ((ce = cudaMalloc(&ws, (NV + 2) * per + sbytes + ND * dbytes)) != cudaSuccess) {
     cudaGetLastError();
     return MPSP_E_NOMEM;
   }
-  void* dwork = dbytes ? (void*)(ws + (NV + 2) * per + sbytes) : nullptr;
+  void* dwk[ND];
+  for (int j = 0; j < ND; ++j) dwk[j] = dbytes ? (void*)(ws + (NV + 2) * per + sbytes + j * dbytes) : nullptr;
+  void* dwork = dwk[0];
+  cudaStream_t dst_[ND] = {};
+  cudaEvent_t dev_[ND + 1] = {};
+  bool conc = true;
+  for (int j = 0; j < ND && conc; ++j)
+    conc = cudaStreamCreateWithFlags(&dst_[j], cudaStreamNonBlocking) == cudaSuccess &&
+           cudaEventCreateWithFlags(&dev_[j], cudaEventDisableTiming) == cudaSuccess;
+  conc = conc && cudaEventCreateWithFlags(&dev_[ND], cudaEventDisableTiming) == cudaSuccess;
+  if (!conc) cudaGetLastError();
   struct V { uint32_t* l; int32_t* e; uint8_t* s; };
   V vec[NV + 2];
   for (int i = 0; i < NV + 2; ++i) {
@@ -915,6 +926,20 @@ int mpsp_gpbicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, con
     K(krylov_dot(L, n, in(a), in(b2), sc_out(slot), fl, st, dwork));
   };
   auto scal = [&](int op) { K(krylov_scalar(L, S, fl, op, st)); };
+  // mu1..mu5: forked onto ND streams (own workspaces), joined back on st
+  auto dot5 = [&](const V* xa, const V* xb, const int* slot) {
+    if (!conc) {
+      for (int j = 0; j < ND; ++j) K(krylov_dot(L, n, in(xa[j]), in(xb[j]), sc_out(slot[j]), fl, st, dwk[j]));
+      return;
+    }
+    K((int)cudaEventRecord(dev_[ND], st));
+    for (int j = 0; j < ND; ++j) {
+      K((int)cudaStreamWaitEvent(dst_[j], dev_[ND], 0));
+      K(krylov_dot(L, n, in(xa[j]), in(xb[j]), sc_out(slot[j]), fl, dst_[j], dwk[j]));
+      K((int)cudaEventRecord(dev_[j], dst_[j]));
+    }
+    for (int j = 0; j < ND; ++j) K((int)cudaStreamWaitEvent(st, dev_[j], 0));
+  };
   {
     std::vector<uint32_t> hl((size_t)KS_N * L, 0u);
     std::vector<int32_t> he(KS_N, 0);
@@ -963,11 +988,11 @@ int mpsp_gpbicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, con
       spmv(t, v);
       ax(KS_ONE, true, q, w, t1);                             // y = s - alpha (w - q)
       ax(KS_ALPHA, true, t1, sv, y);
-      dotv(y, y, KS_MU1);
-      dotv(v, t, KS_MU2);
-      dotv(y, t, KS_MU3);
-      dotv(v, y, KS_MU4);
-      dotv(v, v, KS_MU5);
+      {
+        const V xa[ND] = {y, v, y, v, v}, xb[ND] = {y, t, t, y, v};
+        const int slot[ND] = {KS_MU1, KS_MU2, KS_MU3, KS_MU4, KS_MU5};
+        dot5(xa, xb, slot);
+      }
       scal(7);                                                // tau, zeta, eta
       ax(KS_BETA, false, u, sv, t1);                          // u = zeta q + eta (s + beta u)
       ax(KS_ZETA, false, q, zero, t2);
@@ -991,6 +1016,11 @@ int mpsp_gpbicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, con
     if (hfl[KF_BRK2]) { *status = MPSP_BICG_BREAKDOWN; break; }
   }
   cudaStreamSynchronize(st);
+  for (int j = 0; j < ND; ++j) {
+    if (dst_[j]) cudaStreamDestroy(dst_[j]);
+    if (dev_[j]) cudaEventDestroy(dev_[j]);
+  }
+  if (dev_[ND]) cudaEventDestroy(dev_[ND]);
   cudaFree(ws);
   return rc;
 }
