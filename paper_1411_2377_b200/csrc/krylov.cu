@@ -225,13 +225,18 @@ __global__ void __launch_bounds__(32) dot_chain(int64_t n, DotWork W, int64_t ns
   const int lane = threadIdx.x & 31;
   WChain<L> ch;
   ch.init();
+  // (block b+1's products are loaded while block b is consumed: the lone
+  // chain warp would otherwise wait a full memory latency per block)
   auto sequential = [&](int64_t seg) {
     if (lane == 0) atomicAdd(&g_dot_stats[0], 1ull);
+    const int64_t b0 = seg * DSEG_NB;
+    MP<L> t, tn;
+    if (b0 * 32 < n) load_prod<L>(W, b0, lane, tn);
     for (int b = 0; b < DSEG_NB; ++b) {
-      const int64_t blk = seg * DSEG_NB + b;
+      const int64_t blk = b0 + b;
       if (blk * 32 >= n) break;
-      MP<L> t;
-      load_prod<L>(W, blk, lane, t);
+      t = tn;
+      if (b + 1 < DSEG_NB && (blk + 1) * 32 < n) load_prod<L>(W, blk + 1, lane, tn);
       ch.consume(t, lane);
     }
   };
