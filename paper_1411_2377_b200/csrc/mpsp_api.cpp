@@ -757,8 +757,20 @@ int mpsp_bicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, const
   const size_t sbytes = al((size_t)KS_N * L * 4) + al((size_t)KS_N * 4) + al(KS_N) + 256;
   const size_t dbytes = al(krylov_dot_work_bytes(L, n));
   char* ws = nullptr;
-  if ((ce = cudaMalloc(&ws, 6 * per + sbytes + dbytes)) != cudaSuccess) { cudaGetLastError(); return MPSP_E_NOMEM; }
+  if ((ce = cudaMalloc(&ws, 6 * per + sbytes + 2 * dbytes)) != cudaSuccess) { cudaGetLastError(); return MPSP_E_NOMEM; }
   void* dwork = dbytes ? (void*)(ws + 6 * per + sbytes) : nullptr;
+  void* dwork2 = dbytes ? (void*)(ws + 6 * per + sbytes + dbytes) : nullptr;
+  // (r, r) and the next iteration's rho = (r~, r) are independent: forked
+  // onto two streams (own workspaces) and joined back on st
+  cudaStream_t fs[2] = {};
+  cudaEvent_t fe[3] = {};
+  const char* nf = std::getenv("MPSP_NOFORK");               // tuning knob: 1 = no forked dots
+  bool conc = !(nf && nf[0] == '1');
+  for (int j = 0; j < 2 && conc; ++j)
+    conc = cudaStreamCreateWithFlags(&fs[j], cudaStreamNonBlocking) == cudaSuccess &&
+           cudaEventCreateWithFlags(&fe[j], cudaEventDisableTiming) == cudaSuccess;
+  conc = conc && cudaEventCreateWithFlags(&fe[2], cudaEventDisableTiming) == cudaSuccess;
+  if (!conc) cudaGetLastError();
   struct V { uint32_t* l; int32_t* e; uint8_t* s; };
   V vec[6];
   for (int i = 0; i < 6; ++i) {
@@ -807,11 +819,27 @@ int mpsp_bicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, const
   V xv{x_limbs, x_exps, x_signs};
   cp(bv, r);
   cp(bv, rt);
-  K(krylov_dot(L, n, in(r), in(r), sc_out(KS_RR), fl, st, dwork));
+  // rr = (r, r) -> KS_RR and rho = (r~, r) -> slot `rslot`, concurrently
+  auto rr_rho = [&](int rslot) {
+    if (!conc) {
+      K(krylov_dot(L, n, in(r), in(r), sc_out(KS_RR), fl, st, dwork));
+      K(krylov_dot(L, n, in(rt), in(r), sc_out(rslot), fl, st, dwork2));
+      return;
+    }
+    K((int)cudaEventRecord(fe[2], st));
+    K((int)cudaStreamWaitEvent(fs[0], fe[2], 0));
+    K((int)cudaStreamWaitEvent(fs[1], fe[2], 0));
+    K(krylov_dot(L, n, in(r), in(r), sc_out(KS_RR), fl, fs[0], dwork));
+    K(krylov_dot(L, n, in(rt), in(r), sc_out(rslot), fl, fs[1], dwork2));
+    K((int)cudaEventRecord(fe[0], fs[0]));
+    K((int)cudaEventRecord(fe[1], fs[1]));
+    K((int)cudaStreamWaitEvent(st, fe[0], 0));
+    K((int)cudaStreamWaitEvent(st, fe[1], 0));
+  };
+  rr_rho(KS_RHO);
   K(krylov_scalar(L, S, fl, 0, st));
   int hfl[KF_N] = {0, 0, 0, 0};
   for (int i = 1; i <= max_iter && rc == MPSP_OK; ++i) {
-    K(krylov_dot(L, n, in(rt), in(r), sc_out(KS_RHO), fl, st, dwork));
     K(krylov_scalar(L, S, fl, 1, st));                       // rho == 0 -> stop
     if (i == 1) {
       cp(r, pv);
@@ -832,8 +860,14 @@ int mpsp_bicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, const
     K(krylov_axpy(L, n, sc_in(KS_ALPHA), 0, in(pv), in(xv), out(xv), fl, st));
     K(krylov_axpy(L, n, sc_in(KS_ALPHA), 1, in(z), in(r), out(r), fl, st));
     K(krylov_axpy(L, n, sc_in(KS_ALPHA), 1, in(zt), in(rt), out(rt), fl, st));
-    K(krylov_dot(L, n, in(r), in(r), sc_out(KS_RR), fl, st, dwork));
-    K(krylov_scalar(L, S, fl, 4, st));                       // ||r|| <= thr -> stop
+    rr_rho(KS_TAU);                                          // rr, next rho (KS_TAU: unused here)
+    K(krylov_scalar(L, S, fl, 4, st));                       // ||r|| <= thr -> stop; rho_prev = rho
+    {                                                        // rho := the next rho
+      K((int)cudaMemcpyAsync(S.limbs + (size_t)KS_RHO * L, S.limbs + (size_t)KS_TAU * L, (size_t)L * 4,
+                             cudaMemcpyDeviceToDevice, st));
+      K((int)cudaMemcpyAsync(S.exps + KS_RHO, S.exps + KS_TAU, 4, cudaMemcpyDeviceToDevice, st));
+      K((int)cudaMemcpyAsync(S.signs + KS_RHO, S.signs + KS_TAU, 1, cudaMemcpyDeviceToDevice, st));
+    }
     K((int)cudaMemcpyAsync(hfl, fl, sizeof hfl, cudaMemcpyDeviceToHost, st));
     K((int)cudaStreamSynchronize(st));
     if (rc != MPSP_OK) break;
@@ -842,6 +876,11 @@ int mpsp_bicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, const
     if (hfl[KF_CONV]) { *status = MPSP_BICG_CONVERGED; break; }
   }
   cudaStreamSynchronize(st);
+  for (int j = 0; j < 2; ++j) {
+    if (fs[j]) cudaStreamDestroy(fs[j]);
+    if (fe[j]) cudaEventDestroy(fe[j]);
+  }
+  if (fe[2]) cudaEventDestroy(fe[2]);
   cudaFree(ws);
   return rc;
 }
@@ -876,7 +915,8 @@ int mpsp_gpbicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, con
   void* dwork = dwk[0];
   cudaStream_t dst_[ND] = {};
   cudaEvent_t dev_[ND + 1] = {};
-  bool conc = true;
+  const char* nf = std::getenv("MPSP_NOFORK");               // tuning knob: 1 = no forked dots
+  bool conc = !(nf && nf[0] == '1');
   for (int j = 0; j < ND && conc; ++j)
     conc = cudaStreamCreateWithFlags(&dst_[j], cudaStreamNonBlocking) == cudaSuccess &&
            cudaEventCreateWithFlags(&dev_[j], cudaEventDisableTiming) == cudaSuccess;
