@@ -33,7 +33,11 @@ arithmetic with a single rounding, hand-worked examples and brute force.
 permutation, transpose, small-integer exactness, scaling, negation,
 densification) and by the 1-nnz-row == single rounding property.  The paper
 prints no SpMV values, so whole-config outputs are "parity unpinned by the
-paper" (pinned only through the pieces above).
+paper" (pinned only through the pieces above).  ``dense_mv`` (the paper's
+section-3 dense MP MV) is pinned by closed forms (Lotkin
+row 1 times [1..n] = n(n+1)/2 exactly; A e_j = column j) and by dense ==
+sparse bitwise (tests/test_lotkin.py).  Every function works at any p that is
+a multiple of 32 (the GPU path: 32 ... 8192).
 """
 from __future__ import annotations
 
