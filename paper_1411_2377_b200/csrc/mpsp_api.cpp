@@ -92,6 +92,7 @@ struct mpsp_csr {
   uint32_t flags = 0;
   bool has_t = false;
   bool dense = false;   // mpsp_dense_create: every row holds all n columns
+  mutable const void* ptr_ok[6] = {};   // x/y pointers of the last mpsp_spmv(_t) call that passed the checks
   DevPart A, T;
   // fork/join for running the long-row and short-row kernels concurrently
   cudaStream_t aux = nullptr, aux2 = nullptr;
@@ -313,13 +314,17 @@ int do_spmv(const mpsp_csr* A, bool transpose, const uint32_t* xl, const int32_t
   cudaError_t e = cudaGetDevice(&cur);
   if (e != cudaSuccess) return cuda_fail(e);
   if (cur != A->dev) return MPSP_E_DEVICE;
-  if (check_ptrs) {
+  // (the six pointers of the last call that passed are remembered: a solver
+  // or bench loop re-applying to the same buffers skips the attribute queries)
+  const void* cur6[6] = {xp[0], xp[1], xp[2], yp[0], yp[1], yp[2]};
+  if (check_ptrs && std::memcmp(cur6, A->ptr_ok, sizeof cur6) != 0) {
     for (int i = 0; i < 3; ++i) {
       int rc = n > 0 ? check_device_ptr(xp[i], A->dev) : MPSP_OK;
       if (rc) return rc;
       rc = r > 0 ? check_device_ptr(yp[i], A->dev) : MPSP_OK;
       if (rc) return rc;
     }
+    std::memcpy(A->ptr_ok, cur6, sizeof cur6);
   }
   if (env_validate() && n > 0) {
     std::vector<uint32_t> hl((size_t)n * L);
