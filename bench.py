@@ -233,15 +233,22 @@ def main():
     flush = ws_bytes < 2 * L2_BYTES
     flush_buf = torch.empty(int(2 * L2_BYTES), dtype=torch.uint8, device=dev) if flush else None
 
-    def step():
+    # events created up front: the host work between a step's first event and
+    # its launch stays minimal (the GPU would idle through it)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+            torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.warmup + args.steps)]
+    it_ev = iter(evs)
+
+    def step(ev0=None, ev1=None):
         if world == 1:
             xf = x_full
         elif X is not None:
             xf = X.exchange(x_local)
         else:
             xf = allgather_x(x_local, n)
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0 = ev0 or torch.cuda.Event(enable_timing=True)
+        ev1 = ev1 or torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
         f(xf, out=y, stream=stream)
         ev1.record(stream)
@@ -265,12 +272,11 @@ def main():
     if world > 1:
         dist.barrier()
     for _ in range(args.steps):
+        s0, s1, e0_, e1_ = next(it_ev)
         if flush:
             flush_buf.zero_()          # outside the step events: L2 cold for each step
-        s0 = torch.cuda.Event(enable_timing=True)
-        s1 = torch.cuda.Event(enable_timing=True)
         s0.record(stream)
-        k0, k1 = step()
+        k0, k1 = step(e0_, e1_)
         s1.record(stream)
         kern_ms.append((k0, k1))
         step_ms.append((s0, s1))
