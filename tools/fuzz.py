@@ -107,6 +107,27 @@ def run(seed):
                 MPVec.from_host(*oracle.pack_vec(v, p), device="cuda:0"))
         if not same(g.to_host(), oracle.pack_vec([K.dot(u, v, p)], p)):
             return f"dot p={p} m={m}"
+    if R.random() < 0.1 and p >= 128:                  # a few solver iterations
+        m = R.choice([5, 12, 30])
+        sets = [sorted({i, (i + 1) % m, (i + R.randrange(1, m)) % m}) for i in range(m)]
+        rp = np.zeros(m + 1, np.int64)
+        np.cumsum([len(c) for c in sets], out=rp[1:])
+        ci = [j for c in sets for j in c]
+        vl = [(0, 1 << (p - 1), 5) if j == i else value(R, p, 0)     # dominant diagonal 16
+              for i, c in enumerate(sets) for j in c]
+        A = (rp, np.array(ci, np.int32), *oracle.pack_vec(vl, p))
+        b = [value(R, p, 0) for _ in range(m)]
+        solver = R.choice(["bicg", "gpbicg"])
+        it = R.choice([1, 3, 5])
+        want = (K.bicg if solver == "bicg" else K.gpbicg)(p, A, b, it)
+        H = CSR(p, *A, transpose=(solver == "bicg"))
+        bv = MPVec.from_host(*oracle.pack_vec(b, p), device="cuda:0")
+        xg, itg, st = (H.bicg if solver == "bicg" else H.gpbicg)(bv, it)
+        torch.cuda.synchronize()
+        H.close()
+        if (itg, st) != (want["iters"], want["status"]) or \
+                not same(xg.to_host(), oracle.pack_vec(want["x"], p)):
+            return f"{solver} p={p} m={m} it={it}"
     return None
 
 
