@@ -113,9 +113,12 @@ __device__ __forceinline__ void wcolumns(const uint32_t* sA, const uint32_t* sX,
         } else if (u < v) {                        // i > c: column c + L
           mac64(hi[u], hi2[u], ai, sX[c + L - i]);
         } else if (SHORT) {                        // diagonal chunk, hi part only
-          const bool l = ii <= lane;
-          const uint32_t xv = sX[l ? 0 : c + L - i];
-          mac64(hi[u], hi2[u], ai, l ? 0u : xv);
+          // skewed: lane j takes i2 = 32v + j + 1 + ii, so x[c + L - i2] =
+          // x[L - 1 - ii] is one broadcast word; i2 past the chunk (ii >=
+          // 31 - j) contributes a zero operand
+          const uint32_t a2 = sA[32 * v + lane + 1 + ii];
+          const uint32_t x2 = sX[L - 1 - ii];
+          mac64(hi[u], hi2[u], ii < 31 - lane ? a2 : 0u, x2);
         } else {                                   // diagonal chunk: both
           const bool l = ii <= lane;
           const uint32_t xv = sX[l ? c - i : c + L - i];
@@ -313,25 +316,32 @@ __device__ __forceinline__ void wadd(WMP<K>& s, const WMP<K>& t, uint32_t* ys, i
   }
   // Y (with a guard limb at index 0) shifted right by d: ys[1 + m] = small limb m
   const uint32_t q = (uint32_t)d >> 5, r = (uint32_t)d & 31u;
+  uint32_t y[K], yg = 0u, stk0 = 0u;
+  if (q == 0u) {                                   // d < 32 (warp-uniform): a lane shuffle,
+    const uint32_t nx = __shfl_down_sync(FULL, Y[0], 1);   // nothing below the guard
 #pragma unroll
-  for (int i = 0; i < K; ++i) {
-    ys[1 + lane * K + i] = Y[i];
-    ys[L + 1 + lane * K + i] = 0u;
-  }
-  if (lane == 0) { ys[0] = 0u; ys[2 * L + 1] = 0u; }
-  __syncwarp();
-  uint32_t y[K], yg = 0u;
+    for (int i = 0; i < K; ++i) y[i] = __funnelshift_r(Y[i], i + 1 < K ? Y[i + 1] : (lane < 31 ? nx : 0u), r);
+    if (lane == 0) yg = __funnelshift_r(0u, Y[0], r);
+  } else {
 #pragma unroll
-  for (int i = 0; i < K; ++i) {
-    const int k = lane * K + 1 + i;                // aligned position k (1..L)
-    y[i] = __funnelshift_r(ys[k + q], ys[k + q + 1], r);
+    for (int i = 0; i < K; ++i) {
+      ys[1 + lane * K + i] = Y[i];
+      ys[L + 1 + lane * K + i] = 0u;
+    }
+    if (lane == 0) { ys[0] = 0u; ys[2 * L + 1] = 0u; }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const int k = lane * K + 1 + i;                // aligned position k (1..L)
+      y[i] = __funnelshift_r(ys[k + q], ys[k + q + 1], r);
+    }
+    if (lane == 0) yg = __funnelshift_r(ys[q], ys[q + 1], r);
+    uint32_t orr = 0u;                               // bits below the guard limb
+    for (uint32_t k = lane; k < q; k += 32) orr |= ys[k];
+    if (lane == 0) orr |= ys[q] & ((1u << r) - 1u);
+    stk0 = __ballot_sync(FULL, orr != 0u) != 0u ? 1u : 0u;
+    __syncwarp();                                    // ys reads done
   }
-  if (lane == 0) yg = __funnelshift_r(ys[q], ys[q + 1], r);
-  uint32_t orr = 0u;                               // bits below the guard limb
-  for (uint32_t k = lane; k < q; k += 32) orr |= ys[k];
-  if (lane == 0) orr |= ys[q] & ((1u << r) - 1u);
-  const uint32_t stk0 = __ballot_sync(FULL, orr != 0u) != 0u ? 1u : 0u;
-  __syncwarp();                                    // ys reads done
   // Z + (Y ^ m) + cin over [guard | L limbs]; m = ~0, cin = 1 - stk for a subtraction
   const uint32_t msk = 0u - sub;
   uint32_t zg = 0u, c = 0u;

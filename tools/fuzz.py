@@ -21,7 +21,7 @@ from oracle import krylov as K  # noqa: E402
 from paper_1411_2377_b200 import CSR, MPVec  # noqa: E402
 from paper_1411_2377_b200.csr import dot  # noqa: E402
 
-PS = [32, 64, 128, 256, 512, 1024, 2048, 4096, 8192]
+PS = [int(v) for v in os.environ.get("FUZZ_P", "32,64,128,256,512,1024,2048,4096,8192").split(",")]
 
 
 def value(R, p, e0):
