@@ -109,8 +109,11 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 constexpr int CP_THREADS = 128;
 // (L = 16 with 5 blocks/SM and L = 8 with 8 blocks/SM measured no faster than
 // the register-prefetch kernel, so only L = 32 uses this kernel)
+#ifndef MPSP_CP_MINB
+#define MPSP_CP_MINB 3
+#endif
 template <int L>
-struct CpMinB { static constexpr int v = 3; };
+struct CpMinB { static constexpr int v = MPSP_CP_MINB; };
 
 template <int L>
 __global__ void __launch_bounds__(CP_THREADS, CpMinB<L>::v) spmv_sell_cp(PartView P, XView x, YView y) {
