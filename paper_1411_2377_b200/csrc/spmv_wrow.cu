@@ -16,14 +16,19 @@
 //
 // Per block of 32 entries (one per lane): each lane forms t_k = RN(a_k x_col)
 // (Comba, IMAD.WIDE), aligns it to the grid u, and rounds it (Q_k).  A warp
-// scan of 64-bit high parts h_k = floor(Q_k/H) gives conservative bounds on
-// every partial sum; if all are provably inside [2^(p-1), 2^p - 1] the block
-// commits: each lane adds Q_k to its private (L+2)-limb partial sum R_lane
-// (S = sum over lanes of R, exact mod 2^(32(L+2)), reduced only when needed).
-// Otherwise, at the first failing step f, the steps before f commit, S is
-// reduced exactly (warp butterfly), step f is done by the general adder
-// mp_add (all lanes redundantly), and the block resumes at f+1 with the new
-// binade.  Nothing is approximated: the bounds only decide fast vs exact.
+// scan of int32 high parts h_k = floor(Q_k/H) (H = 2^(p-26) grid units)
+// gives conservative bounds on every partial sum; if all are provably inside
+// [2^(p-1), 2^p - 1] the block commits: each lane adds Q_k to its private
+// (L+2)-limb partial sum R_lane (S = sum over lanes of R, exact mod
+// 2^(32(L+2)), reduced only when needed).  Otherwise, at the first failing
+// step f, the steps before f commit; a step that provably moves the sum one
+// binade up or down, or whose product dominates the sum, is rounded on the
+// certified new grid from ballots / one redux over the lanes' R (WChain's
+// transitions); any other failing step reduces S exactly (warp butterfly),
+// runs the general adder mp_add (all lanes redundantly), and the block
+// resumes at f+1 in the new binade.  Nothing is approximated: the bounds
+// only decide fast vs exact (wchain.cuh; CPU model in
+// tests/test_kernel_algorithms.py).
 #include <cuda_runtime.h>
 
 #include <climits>
