@@ -1,10 +1,13 @@
-// krylov.cu - multiple-precision BiCG on the GPU:
-// PAPER.md:249-297 (Fig. 4, BiCG) with K = I, the two SpMVs (A p, A^T p~)
-// by this library's kernels, and PAPER.md:375-380 (convergence test
+// krylov.cu - multiple-precision BiCG and GPBiCG on the GPU (SURVEY.md 8(f)
+// ranks 1-2): PAPER.md:249-369 (Fig. 4) with K = I, the SpMVs by this
+// library's kernels, and PAPER.md:375-380 (convergence test
 // ||r|| <= 1e-20 ||r_0|| + 1e-50).  Every operation is one p-bit RN
-// operation in the order the figure writes it (readings c26-c31):
+// operation in the order the figure writes it (readings c26-c35);
+// p > 1024 runs the same steps on warp-distributed values (krylov_wide.cu).
 //   dot      (u, v) = ordered chain s = RN(s + RN(u_k v_k)), k ascending
-//            (one warp, the exact speculative block sum of wchain.cuh)
+//            (segments evaluated speculatively in parallel and validated in
+//            order by one warp; the exact speculative block sum of
+//            wchain.cuh for the segments that do not validate)
 //   axpy     z_k = RN(y_k + RN(+-alpha x_k))            (thread per element)
 //   scalars  RN(a / b), RN(sqrt(a)), exact compare      (one thread:
 //            integer long division / square root + one rounding)
