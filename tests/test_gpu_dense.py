@@ -63,3 +63,23 @@ def test_dense_row_block_and_errors():
         CSR.dense(256, 90, bad, d["dense_exps"], d["dense_signs"])
     with pytest.raises(MpspError):
         CSR.dense(256, 50000, np.zeros((1, 8), np.uint32), np.zeros(1, np.int32), np.zeros(1, np.uint8))
+
+
+@pytest.mark.parametrize("p", [256, 2048])
+def test_dense_empty_and_single(p):
+    """n = 0 (nothing to do) and n = 1 (one product, RN(+0 + t) = t)."""
+    from paper_1411_2377_b200 import CSR, MPVec
+    L = p // 32
+    D = CSR.dense(p, 0, np.zeros((0, L), np.uint32), np.zeros(0, np.int32), np.zeros(0, np.uint8))
+    x = MPVec.from_host(np.zeros((0, L), np.uint32), np.zeros(0, np.int32), np.zeros(0, np.uint8),
+                        device="cuda:0")
+    y = D.spmv(x).to_host()
+    assert y[0].size == 0
+    D.close()
+    d = LK.make(1, 0, p)
+    D = CSR.dense(p, 1, d["dense_limbs"], d["dense_exps"], d["dense_signs"])
+    x = MPVec.from_host(d["x_limbs"], d["x_exps"], d["x_signs"], device="cuda:0")
+    want = oracle.dense_mv(p, 1, d["dense_limbs"], d["dense_exps"], d["dense_signs"],
+                           d["x_limbs"], d["x_exps"], d["x_signs"])
+    assert_same(D.spmv(x).to_host(), want, "n=1")
+    D.close()
