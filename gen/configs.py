@@ -72,22 +72,26 @@ def pack_triples(vals, p):
 
 # ------------------------------------------------------------------ patterns
 def _dedupe_sorted(rng, rows, cols, lo, hi, skip_diag):
-    """Make columns distinct within each row (resample duplicates), sorted."""
+    """Make columns distinct within each row (resample duplicates), sorted.
+
+    Entries are ordered by the single key row * K + col (K > every column):
+    the same order as lexsort((cols, rows)), one int64 sort per round."""
+    K = np.int64(max(int(hi), int(cols.max()) + 1 if len(cols) else 1))
+    key = np.sort(rows * K + cols)
     while True:
-        order = np.lexsort((cols, rows))
-        cols = cols[order]
-        rows = rows[order]
-        dup = np.zeros(len(cols), dtype=bool)
-        if len(cols) > 1:
-            dup[1:] = (cols[1:] == cols[:-1]) & (rows[1:] == rows[:-1])
+        dup = np.zeros(len(key), dtype=bool)
+        if len(key) > 1:
+            dup[1:] = key[1:] == key[:-1]
         nd = int(dup.sum())
         if nd == 0:
-            return rows, cols
+            return key // K, key % K
+        r = key[dup] // K
         new = rng.integers(lo, hi, size=nd, dtype=np.int64)
         if skip_diag:
-            new = new + (new >= rows[dup])
-        cols = cols.copy()
-        cols[dup] = new
+            new = new + (new >= r)
+        key = key.copy()
+        key[dup] = r * K + new
+        key = np.sort(key)
 
 
 def pattern_diag_plus_random(rng, n, k_off):

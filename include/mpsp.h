@@ -132,6 +132,11 @@ int mpsp_dense_create(mpsp_csr **out, int p_bits, int64_t n,
  * are caller-owned and must stay alive until the stream work completes.
  * x contents are not validated (an unnormalised nonzero x is undefined
  * behaviour) unless the environment variable MPSP_VALIDATE=1 is set.
+ * The pointer checks (device memory on the handle's device) are skipped when
+ * the six x/y pointers equal those of the handle's last call that passed
+ * them; a caller that frees buffers and passes a new allocation at the same
+ * address without it being device memory of that device must set
+ * MPSP_PTR_CACHE=0 (check every call).
  *
  * Errors: MPSP_E_ARG, MPSP_E_ALIAS, MPSP_E_DEVICE, MPSP_E_VALUE (validation
  * mode only), MPSP_E_CUDA (launch failure).
@@ -182,6 +187,25 @@ const char *mpsp_last_cuda_error(void);
  * Errors: MPSP_E_ARG.
  */
 int mpsp_csr_info(const mpsp_csr *A, int64_t info[10]);
+
+/* ---- x exchange records (multi-GPU) ---------
+ * Before each multi-GPU application x must be replicated wherever a rank's
+ * rows read it (BASELINE.json north_star (4): NCCL over NVLink).  To move
+ * each element as ONE record - one NCCL call per peer, or one all-gather,
+ * instead of three - an element is packed into L + 1 uint32 words: its L limbs
+ * then expw = (sign << 31) | (exp & 0x7fffffff).  Bit-exact for every valid
+ * value (|exp| <= 2^29).  All pointers are DEVICE pointers; asynchronous on
+ * cuda_stream.
+ *
+ * mpsp_vec_pack   - rec[i*(L+1) ..] <- element i of (limbs, exps, signs),
+ *                   i in [0, count).
+ * mpsp_vec_unpack - element i of (limbs, exps, signs) <- rec[i*(L+1) ..].
+ * Errors: MPSP_E_PREC (p not supported), MPSP_E_ARG (count < 0, null
+ * pointer), MPSP_E_ALIAS (record and vector storage overlap), MPSP_E_CUDA. */
+int mpsp_vec_pack(int p_bits, int64_t count, const uint32_t *limbs, const int32_t *exps,
+                  const uint8_t *signs, uint32_t *rec, void *cuda_stream);
+int mpsp_vec_unpack(int p_bits, int64_t count, const uint32_t *rec, uint32_t *limbs,
+                    int32_t *exps, uint8_t *signs, void *cuda_stream);
 
 /* Number of kernels this library has launched in this process (monotone). */
 int64_t mpsp_launch_count(void);

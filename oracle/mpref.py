@@ -209,6 +209,24 @@ def transpose(n, rowptr, colidx):
             np.array(perm, dtype=np.int64))
 
 
+def transpose_np(n, rowptr, colidx):
+    """The same transpose as ``transpose`` (step 5) with numpy's stable sort.
+
+    A stable argsort of the entries by column keeps, inside each column, the
+    CSR storage order - ascending row index of A (BASELINE.json north_star
+    (3)).  A library sort primitive, for full-size inputs where sorting
+    Python tuples would take minutes; pinned against ``transpose`` in
+    tests/test_oracle_invariants.py.  Returns (rowptr_t, colidx_t, perm).
+    """
+    rowptr = np.asarray(rowptr, dtype=np.int64)
+    colidx = np.asarray(colidx, dtype=np.int64)
+    perm = np.argsort(colidx, kind='stable').astype(np.int64)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rowptr))   # row i of entry k
+    rowptr_t = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(colidx, minlength=n), out=rowptr_t[1:])
+    return rowptr_t, rows[perm].astype(np.int32), perm
+
+
 def spmv_t(p, rowptr, colidx, limbs, exps, signs, x_limbs, x_exps, x_signs):
     """y = A^T x: y_j = chain over i ascending with (i, j) stored of RN(A_ij x_i)."""
     n = len(rowptr) - 1

@@ -2,6 +2,7 @@
 the library exposes a plain C ABI, include/mpsp.h)."""
 from __future__ import annotations
 
+import fcntl
 import os
 import shutil
 import subprocess
@@ -17,7 +18,7 @@ BUILD = os.path.join(PKG, "build")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["spmv_kernels.cu", "spmv_wrow.cu", "spmv_wide.cu", "krylov.cu", "krylov_wide.cu", "mpsp_api.cpp"]
+SOURCES = ["spmv_kernels.cu", "spmv_wrow.cu", "spmv_wide.cu", "krylov.cu", "krylov_wide.cu", "xchg.cu", "mpsp_api.cpp"]
 
 
 def nvcc() -> str:
@@ -36,10 +37,26 @@ def _deps_mtime() -> float:
 
 
 def build(force: bool = False, verbose: bool = False, defines=(), name: str = "libmpsp.so") -> str:
-    """Compile the library; `defines`/`name` build a tuning variant beside it."""
+    """Compile the library; `defines`/`name` build a tuning variant beside it.
+
+    Safe to call from every rank of a torchrun job at once: an exclusive file
+    lock serialises the builders, so the first one compiles and the others
+    find the library current when they get the lock."""
     lib = os.path.join(PKG, name)
     if not force and os.path.exists(lib) and os.path.getmtime(lib) >= _deps_mtime():
         return lib
+    os.makedirs(BUILD, exist_ok=True)
+    with open(os.path.join(BUILD, name + ".lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        try:
+            if not force and os.path.exists(lib) and os.path.getmtime(lib) >= _deps_mtime():
+                return lib
+            return _compile(lib, verbose, defines, name)
+        finally:
+            fcntl.flock(lk, fcntl.LOCK_UN)
+
+
+def _compile(lib, verbose, defines, name):
     bdir = BUILD if name == "libmpsp.so" else os.path.join(BUILD, name)
     os.makedirs(bdir, exist_ok=True)
     nv = nvcc()
@@ -58,7 +75,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), name: str = "l
 
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    tmp = lib + ".tmp"
+    tmp = f"{lib}.{os.getpid()}.tmp"
     cmd = [nv, *ARCH, "-shared", "--cudart", "shared", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

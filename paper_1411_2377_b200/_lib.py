@@ -24,7 +24,8 @@ ERROR_CODES = {v: k for k, v in ERRORS.items()}
 SYMBOLS = ("mpsp_csr_create", "mpsp_dense_create", "mpsp_spmv", "mpsp_spmv_t", "mpsp_spmv_host", "mpsp_spmv_t_host",
            "mpsp_destroy", "mpsp_strerror", "mpsp_last_cuda_error", "mpsp_csr_info",
            "mpsp_launch_count", "mpsp_imad_bench", "mpsp_supported_precision",
-           "mpsp_dot", "mpsp_axpy", "mpsp_bicg", "mpsp_gpbicg", "mpsp_debug_dot_stats")
+           "mpsp_dot", "mpsp_axpy", "mpsp_bicg", "mpsp_gpbicg", "mpsp_debug_dot_stats",
+           "mpsp_vec_pack", "mpsp_vec_unpack")
 BICG_STATUS = {0: "converged", 1: "breakdown", 2: "max_iter"}
 
 
@@ -88,6 +89,10 @@ def lib() -> ctypes.CDLL:
     L.mpsp_gpbicg.restype = I
     L.mpsp_debug_dot_stats.argtypes = [P]
     L.mpsp_debug_dot_stats.restype = I
+    L.mpsp_vec_pack.argtypes = [I, I64, P, P, P, P, P]
+    L.mpsp_vec_pack.restype = I
+    L.mpsp_vec_unpack.argtypes = [I, I64, P, P, P, P, P]
+    L.mpsp_vec_unpack.restype = I
     _lib = L
     return L
 

@@ -18,6 +18,27 @@ except ImportError:  # pragma: no cover
     torch = None
 
 
+def check_vec(v: "MPVec", n: int, L: int, name: str, device=None) -> None:
+    """Raise ValueError unless v is an n-element, L-limb MPVec of int32 /
+    int32 / uint8 contiguous CUDA tensors (on `device` if given): the C ABI
+    takes raw pointers and cannot check sizes itself."""
+    if not isinstance(v, MPVec):
+        raise ValueError(f"{name}: expected an MPVec, got {type(v).__name__}")
+    l, e, s = v.limbs, v.exps, v.signs
+    if l.dim() != 2 or tuple(l.shape) != (n, L) or tuple(e.shape) != (n,) or tuple(s.shape) != (n,):
+        raise ValueError(f"{name}: shape limbs {tuple(l.shape)} exps {tuple(e.shape)} signs "
+                         f"{tuple(s.shape)}, expected ({n}, {L}) / ({n},) / ({n},)")
+    if l.dtype != torch.int32 or e.dtype != torch.int32 or s.dtype != torch.uint8:
+        raise ValueError(f"{name}: dtypes {l.dtype}/{e.dtype}/{s.dtype}, expected int32/int32/uint8")
+    if not (l.is_contiguous() and e.is_contiguous() and s.is_contiguous()):
+        raise ValueError(f"{name}: tensors must be contiguous")
+    devs = {l.device, e.device, s.device}
+    if len(devs) != 1 or next(iter(devs)).type != "cuda":
+        raise ValueError(f"{name}: tensors must live on one CUDA device, got {devs}")
+    if device is not None and l.device != torch.device(device):
+        raise ValueError(f"{name}: on {l.device}, expected {device}")
+
+
 def _ptr(a) -> int:
     if a is None:
         return 0
@@ -122,8 +143,10 @@ class CSR:
         return dict(zip(keys, [int(v) for v in arr]))
 
     def _apply(self, fn, x: MPVec, out: MPVec | None, stream) -> MPVec:
+        check_vec(x, self.n, self.L, "x")
         if out is None:
             out = MPVec.empty(self.rows, self.L, device=x.limbs.device)
+        check_vec(out, self.rows, self.L, "out", device=x.limbs.device)
         if stream is None:
             stream = torch.cuda.current_stream(x.limbs.device).cuda_stream
         elif hasattr(stream, "cuda_stream"):
@@ -142,13 +165,21 @@ class CSR:
         return self._apply(_lib.lib().mpsp_spmv_t, x, out, stream)
 
     def _host(self, fn, xl, xe, xs, out=None):
-        xl = np.ascontiguousarray(xl, dtype=np.uint32)
+        xl = np.ascontiguousarray(xl, dtype=np.uint32).reshape(-1)
         xe = np.ascontiguousarray(xe, dtype=np.int32)
         xs = np.ascontiguousarray(xs, dtype=np.uint8)
+        if xl.size != self.n * self.L or xe.shape != (self.n,) or xs.shape != (self.n,):
+            raise ValueError(f"x: expected {self.n} elements of {self.L} limbs")
         if out is None:
             out = (np.empty((self.rows, self.L), np.uint32), np.empty(self.rows, np.int32),
                    np.empty(self.rows, np.uint8))
         yl, ye, ys = out
+        for a, dt, size in ((yl, np.uint32, self.rows * self.L), (ye, np.int32, self.rows),
+                            (ys, np.uint8, self.rows)):
+            if not isinstance(a, np.ndarray) or a.dtype != dt or a.size != size or \
+                    not a.flags.c_contiguous:
+                raise ValueError(f"out: expected contiguous {np.dtype(dt).name} arrays of "
+                                 f"{self.rows} rows x {self.L} limbs")
         rc = fn(self._h, _ptr(xl), _ptr(xe), _ptr(xs), _ptr(yl), _ptr(ye), _ptr(ys))
         _lib.check(rc, fn.__name__)
         return out
@@ -174,8 +205,10 @@ class CSR:
         return self._solve(_lib.lib().mpsp_bicg, b, max_iter, x, stream)
 
     def _solve(self, fn, b, max_iter, x, stream):
+        check_vec(b, self.n, self.L, "b")
         if x is None:
             x = MPVec.empty(self.n, self.L, device=b.limbs.device)
+        check_vec(x, self.n, self.L, "x", device=b.limbs.device)
         if stream is None:
             stream = torch.cuda.current_stream(b.limbs.device).cuda_stream
         it, st = ctypes.c_int(0), ctypes.c_int(0)
@@ -213,8 +246,11 @@ def _stream(dev, stream):
 def dot(p: int, u: MPVec, v: MPVec, out: MPVec | None = None, stream=None) -> MPVec:
     """(u, v) as the ordered rounded chain (mpsp_dot); a 1-element MPVec."""
     L = p // 32
+    check_vec(u, u.n, L, "u")
+    check_vec(v, u.n, L, "v", device=u.limbs.device)
     if out is None:
         out = MPVec.empty(1, L, device=u.limbs.device)
+    check_vec(out, 1, L, "out", device=u.limbs.device)
     rc = _lib.lib().mpsp_dot(int(p), u.n, _ptr(u.limbs), _ptr(u.exps), _ptr(u.signs),
                              _ptr(v.limbs), _ptr(v.exps), _ptr(v.signs), _ptr(out.limbs),
                              _ptr(out.exps), _ptr(out.signs),
@@ -226,8 +262,13 @@ def dot(p: int, u: MPVec, v: MPVec, out: MPVec | None = None, stream=None) -> MP
 def axpy(p: int, alpha: MPVec, x: MPVec, y: MPVec, negate: bool = False,
          out: MPVec | None = None, stream=None) -> MPVec:
     """out_k = RN(y_k + RN(+-alpha x_k)) (mpsp_axpy); alpha a 1-element MPVec."""
+    L = p // 32
+    check_vec(alpha, 1, L, "alpha", device=x.limbs.device)
+    check_vec(x, x.n, L, "x")
+    check_vec(y, x.n, L, "y", device=x.limbs.device)
     if out is None:
-        out = MPVec.empty(x.n, p // 32, device=x.limbs.device)
+        out = MPVec.empty(x.n, L, device=x.limbs.device)
+    check_vec(out, x.n, L, "out", device=x.limbs.device)
     rc = _lib.lib().mpsp_axpy(int(p), x.n, _ptr(alpha.limbs), _ptr(alpha.exps), _ptr(alpha.signs),
                               1 if negate else 0, _ptr(x.limbs), _ptr(x.exps), _ptr(x.signs),
                               _ptr(y.limbs), _ptr(y.exps), _ptr(y.signs), _ptr(out.limbs),

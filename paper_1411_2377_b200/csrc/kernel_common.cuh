@@ -3,12 +3,36 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "layout.h"
 #include "mp_device.cuh"
 
 namespace mpsp {
+
+// cudaFuncSetAttribute applies to the CURRENT device only: the opt-in to more
+// than 48 KB of dynamic shared memory is remembered per device ordinal (a
+// process may hold handles on several GPUs).
+inline int ensure_smem_attr(const void* fn, size_t bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return (int)e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (dev < 64 && (done.load(std::memory_order_relaxed) & bit)) return 0;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return (int)e;
+  if (dev < 64) done.fetch_or(bit);
+  return 0;
+}
+
+// SM count of the current device (the runtime caches the attribute)
+inline int current_sms() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
 
 template <int L>
 struct Chunk;  // CW-word vector type

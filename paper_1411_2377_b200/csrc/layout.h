@@ -109,6 +109,12 @@ enum { KS_RHO, KS_RHOP, KS_SIGMA, KS_ALPHA, KS_BETA, KS_RR, KS_NRM, KS_THR, KS_C
        KS_N };
 // KF_BRK2: breakdown detected after the iteration's update (GPBiCG zeta = 0)
 enum { KF_STOP, KF_BREAK, KF_CONV, KF_BRK2, KF_N };
+// x exchange records (xchg.cu): pack count elements into (L+1)-word records
+// (L limbs + expw) or unpack records into an ABI vector; cudaError_t value.
+int launch_vec_pack(int L, bool unpack, int64_t count, const uint32_t* limbs_in,
+                    const int32_t* exps_in, const uint8_t* signs_in, const uint32_t* rec_in,
+                    uint32_t* rec_out, uint32_t* limbs_out, int32_t* exps_out, uint8_t* signs_out,
+                    void* stream);
 // Integer-MAC microbenchmark (roofline denominator); returns cudaError_t.
 int run_imad_bench(double out[3]);
 // Launches this process has made.

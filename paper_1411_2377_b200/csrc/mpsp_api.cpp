@@ -315,9 +315,15 @@ int do_spmv(const mpsp_csr* A, bool transpose, const uint32_t* xl, const int32_t
   if (e != cudaSuccess) return cuda_fail(e);
   if (cur != A->dev) return MPSP_E_DEVICE;
   // (the six pointers of the last call that passed are remembered: a solver
-  // or bench loop re-applying to the same buffers skips the attribute queries)
+  // or bench loop re-applying to the same buffers skips the attribute
+  // queries.  MPSP_PTR_CACHE=0 queries on every call - for callers that free
+  // and re-allocate buffers between calls, include/mpsp.h)
   const void* cur6[6] = {xp[0], xp[1], xp[2], yp[0], yp[1], yp[2]};
-  if (check_ptrs && std::memcmp(cur6, A->ptr_ok, sizeof cur6) != 0) {
+  static const bool no_cache = [] {
+    const char* v = std::getenv("MPSP_PTR_CACHE");
+    return v && v[0] == '0';
+  }();
+  if (check_ptrs && (no_cache || std::memcmp(cur6, A->ptr_ok, sizeof cur6) != 0)) {
     for (int i = 0; i < 3; ++i) {
       int rc = n > 0 ? check_device_ptr(xp[i], A->dev) : MPSP_OK;
       if (rc) return rc;
@@ -640,6 +646,45 @@ int mpsp_spmv_host(mpsp_csr* A, const uint32_t* x_limbs, const int32_t* x_exps,
 int mpsp_spmv_t_host(mpsp_csr* A, const uint32_t* x_limbs, const int32_t* x_exps,
                      const uint8_t* x_signs, uint32_t* y_limbs, int32_t* y_exps, uint8_t* y_signs) {
   return spmv_host(A, true, x_limbs, x_exps, x_signs, y_limbs, y_exps, y_signs);
+}
+
+static int vec_pack_impl(int p_bits, int64_t count, bool unpack, const uint32_t* limbs_in,
+                         const int32_t* exps_in, const uint8_t* signs_in, const uint32_t* rec_in,
+                         uint32_t* rec_out, uint32_t* limbs_out, int32_t* exps_out,
+                         uint8_t* signs_out, void* stream) {
+  if (!mpsp_supported_precision(p_bits)) return MPSP_E_PREC;
+  if (count < 0) return MPSP_E_ARG;
+  if (count == 0) return MPSP_OK;
+  const int L = p_bits / 32;
+  const void* ptrs[4] = {unpack ? (const void*)rec_in : (const void*)limbs_in,
+                         unpack ? (const void*)limbs_out : (const void*)exps_in,
+                         unpack ? (const void*)exps_out : (const void*)signs_in,
+                         unpack ? (const void*)signs_out : (const void*)rec_out};
+  for (const void* q : ptrs)
+    if (!q) return MPSP_E_ARG;
+  const size_t rb = (size_t)count * (L + 1) * 4;
+  if (unpack ? (overlap(rec_in, rb, limbs_out, (size_t)count * L * 4) ||
+                overlap(rec_in, rb, exps_out, (size_t)count * 4) ||
+                overlap(rec_in, rb, signs_out, (size_t)count))
+             : (overlap(rec_out, rb, limbs_in, (size_t)count * L * 4) ||
+                overlap(rec_out, rb, exps_in, (size_t)count * 4) ||
+                overlap(rec_out, rb, signs_in, (size_t)count)))
+    return MPSP_E_ALIAS;
+  const int e = launch_vec_pack(L, unpack, count, limbs_in, exps_in, signs_in, rec_in, rec_out,
+                                limbs_out, exps_out, signs_out, stream);
+  return e ? cuda_fail((cudaError_t)e) : MPSP_OK;
+}
+
+int mpsp_vec_pack(int p_bits, int64_t count, const uint32_t* limbs, const int32_t* exps,
+                  const uint8_t* signs, uint32_t* rec, void* cuda_stream) {
+  return vec_pack_impl(p_bits, count, false, limbs, exps, signs, nullptr, rec, nullptr, nullptr,
+                       nullptr, cuda_stream);
+}
+
+int mpsp_vec_unpack(int p_bits, int64_t count, const uint32_t* rec, uint32_t* limbs,
+                    int32_t* exps, uint8_t* signs, void* cuda_stream) {
+  return vec_pack_impl(p_bits, count, true, nullptr, nullptr, nullptr, rec, nullptr, limbs, exps,
+                       signs, cuda_stream);
 }
 
 int mpsp_csr_info(const mpsp_csr* A, int64_t info[10]) {

@@ -210,13 +210,8 @@ static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStrea
     if (!(vc && vc[0] == '0')) {
       constexpr int NC = L / 4;
       const size_t smem = (size_t)4 * NC * CP_THREADS * 16;   // 2 stages x (a, x): 16L KB
-      static bool attr = false;
-      if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(spmv_sell_cp<L>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return (int)e;
-        attr = true;
-      }
+      static std::atomic<uint64_t> attr{0};
+      if (int e = ensure_smem_attr((const void*)spmv_sell_cp<L>, smem, attr)) return e;
       spmv_sell_cp<L><<<(unsigned)blocks, CP_THREADS, smem, st>>>(P, x, y);
       g_launches.fetch_add(1);
       return (int)cudaGetLastError();
@@ -231,12 +226,7 @@ static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStrea
   const char* vm = std::getenv("MPSP_MINB");
   int minb = L == 16 ? 4 : 1;
   if (L <= 8) {
-    static int sms = 0;
-    if (sms == 0) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = current_sms();
     minb = (blocks > (int64_t)sms * 5 && blocks <= (int64_t)sms * 6) ? 6 : 5;
   }
   if (vm) minb = std::atoi(vm);

@@ -90,12 +90,8 @@ int launch(const PartView& P, const XView& x, const YView& y, cudaStream_t st) {
   if (P.nwrow <= 0) return 0;
   constexpr int L = 32 * K;
   const size_t smem = (size_t)WARPS * 8 * L * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(spmv_wide<K, DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return (int)e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (int e = ensure_smem_attr((const void*)spmv_wide<K, DENSE>, smem, attr)) return e;
   const int64_t blocks = (P.nwrow + WARPS - 1) / WARPS;
   spmv_wide<K, DENSE><<<(unsigned)blocks, 32 * WARPS, smem, st>>>(P, x, y);
   launch_counter_add(1);

@@ -401,13 +401,8 @@ static int launch_pcrow_L(const PartView& P, const XView& x, const YView& y, cud
   if (P.npcrow <= 0) return 0;
   constexpr int U = pc_spl(L);
   const size_t smem = 2 * sizeof(PcSlot<L, U>) + 16;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(spmv_pcrow<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return (int)e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (int e = ensure_smem_attr((const void*)spmv_pcrow<L>, smem, attr)) return e;
   spmv_pcrow<L><<<(unsigned)P.npcrow, 32 * (1 + U), smem, st>>>(P, x, y);
   launch_counter_add(1);
   return (int)cudaGetLastError();

@@ -196,13 +196,15 @@ def test_needed_window_suffices(cfg, n, op):
     """Emulated G-rank run on one GPU: each rank's x buffer holds the global x
     only inside its needed window (dist.needed_window) and junk everywhere
     else; the concatenated row blocks must equal the 1-GPU result, i.e. the
-    kernels never read x outside the window the exchange fills."""
+    kernels never read x outside the window the exchange fills.  Compared
+    with the oracle (and the 1-GPU CUDA result), not with the CUDA path alone."""
     import torch
     from paper_1411_2377_b200 import MPVec
     from paper_1411_2377_b200.dist import block_range, needed_window
     d = gen.make(cfg, n=n, seed=13)
     n = d["n"]
-    full = gpu_run(d, op)
+    full = oracle_full(d, op)
+    assert_same(gpu_run(d, op), full, f"{cfg} 1-GPU {op}")
     rng = np.random.default_rng(5)
     for G in (2, 4, 8):
         parts = []
@@ -238,7 +240,7 @@ def test_distcsr_single_rank_nccl(exchange):
     port = s.getsockname()[1]
     s.close()
     d = gen.make("C5", n=2500, seed=14)
-    want = gpu_run(d, "ax")
+    want = oracle_full(d, "ax")
     dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
                             device_id=torch.device("cuda", 0))
     try:
@@ -251,3 +253,84 @@ def test_distcsr_single_rank_nccl(exchange):
         D.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("p", [32, 64, 128, 256, 1024, 2048])
+def test_vec_pack_unpack_records(p):
+    """mpsp_vec_pack / mpsp_vec_unpack (the x-exchange records, csrc/xchg.cu):
+    record i = (L limbs, (sign << 31) | (exp & 0x7fffffff)), built here with
+    numpy; unpack restores the vector bit for bit."""
+    import torch
+    from paper_1411_2377_b200 import MPVec
+    from paper_1411_2377_b200.dist import LibPacker
+    L = p // 32
+    rng = np.random.default_rng(p)
+    n = 3001
+    xl = rng.integers(0, 2 ** 32, size=(n, L), dtype=np.uint32)
+    xe = rng.integers(-(2 ** 29), 2 ** 29 + 1, size=n).astype(np.int32)
+    xs = rng.integers(0, 2, size=n).astype(np.uint8)
+    v = MPVec.from_host(xl, xe, xs, device="cuda:0")
+    rec = torch.zeros((n, L + 1), dtype=torch.int32, device="cuda:0")
+    P = LibPacker(L)
+    P.pack(v, rec)
+    want = np.zeros((n, L + 1), np.uint32)
+    want[:, :L] = xl
+    want[:, L] = (xs.astype(np.uint32) << 31) | (xe.view(np.uint32) & np.uint32(0x7fffffff))
+    torch.cuda.synchronize()
+    assert np.array_equal(rec.cpu().numpy().view(np.uint32), want)
+    w = MPVec.empty(n, L, device="cuda:0")
+    P.unpack(rec, w)
+    torch.cuda.synchronize()
+    gl, ge, gs = w.to_host()
+    assert np.array_equal(gl, xl) and np.array_equal(ge, xe) and np.array_equal(gs, xs)
+
+
+@pytest.mark.parametrize("cfg,n,op", [("C5", 4900, "ax"), ("C2", 5000, "ax"), ("C2", 5000, "atx"),
+                                      ("C4", 6000, "ax")])
+def test_interior_boundary_split_emulated(cfg, n, op):
+    """DistCSR's overlap split, emulated for G ranks on one GPU: each rank's
+    rows are cut into boundary / interior / boundary row-range handles
+    (dist.interior_mask / interior_run); the interior rows run with x valid
+    ONLY inside the own block (junk elsewhere - as while the exchange is in
+    flight), the boundary rows with x valid inside the needed window.  The
+    concatenation must equal the oracle's result."""
+    import torch
+    from paper_1411_2377_b200 import MPVec
+    from paper_1411_2377_b200.dist import block_range, interior_mask, interior_run, needed_window
+    d = gen.make(cfg, n=n, seed=21)
+    n = d["n"]
+    tr = op == "atx"
+    want = oracle_full(d, op)
+    rng = np.random.default_rng(9)
+
+    def junk_x(valid):
+        xl = rng.integers(0, 2 ** 32, size=d["x_limbs"].shape, dtype=np.uint32)
+        xe = rng.integers(-2 ** 20, 2 ** 20, size=n).astype(np.int32)
+        xs = rng.integers(0, 2, size=n).astype(np.uint8)
+        xl[:, -1] |= np.uint32(0x80000000)
+        a, b = valid
+        xl[a:b], xe[a:b], xs[a:b] = d["x_limbs"][a:b], d["x_exps"][a:b], d["x_signs"][a:b]
+        return MPVec.from_host(xl, xe, xs, device="cuda:0")
+
+    for G in (2, 4, 8):
+        parts, n_inner = [], 0
+        for r in range(G):
+            rb, re = block_range(n, G, r)
+            a, b = interior_run(interior_mask(d["rowptr"], d["colidx"], rb, re, transpose=tr))
+            win = needed_window(d["rowptr"], d["colidx"], rb, re, transpose=tr)
+            y = MPVec.empty(re - rb, d["p"] // 32, device="cuda:0")
+            x_own, x_win = junk_x((rb, re)), junk_x(win)
+            for c0, c1, inner in ((rb, rb + a, False), (rb + a, rb + b, True), (rb + b, re, False)):
+                if c1 <= c0:
+                    continue
+                A = _csr(d, rows=(c0, c1), transpose=tr)
+                ys = MPVec(y.limbs[c0 - rb:c1 - rb], y.exps[c0 - rb:c1 - rb], y.signs[c0 - rb:c1 - rb])
+                (A.spmv_t if tr else A.spmv)(x_own if inner else x_win, out=ys)
+                torch.cuda.synchronize()
+                A.close()
+                n_inner += (c1 - c0) if inner else 0
+            parts.append(y.to_host())
+        cat = tuple(np.concatenate([p_[i] for p_ in parts]) for i in range(3))
+        assert_same(cat, want, f"{cfg} G={G} {op} interior/boundary")
+        if cfg in ("C5", "C2"):
+            assert n_inner > n // 2            # banded / stencil blocks are mostly interior
