@@ -25,14 +25,14 @@
 
 namespace mpsp {
 
-// Producer/consumer rows (spmv_pcrow): the chain warp's lane k owns the U
-// consecutive steps Uk .. Uk+U-1 of each 32U-step chunk.  Step j of such a row
-// (chunk c = j/(32U), q = j%(32U)) is stored at position c*32U + 32(q%U) +
-// q/U, so producer warp u's 32 loads of a chunk are consecutive entries.
-#ifndef MPSP_PC_U
-#define MPSP_PC_U 4
+// Warp rows (spmv_wrow): lane k of the row's warp owns the U = wrow_spl(L)
+// consecutive steps Uk .. Uk+U-1 of each 32U-step chunk.  Step j of such a
+// row (chunk c = j/(32U), q = j%(32U)) is stored at position c*32U +
+// 32(q%U) + q/U, so the warp's 32 loads of one u are consecutive entries.
+#ifndef MPSP_WU
+#define MPSP_WU 1
 #endif
-__host__ __device__ constexpr int pc_spl(int L) { return L <= 8 ? MPSP_PC_U : (L <= 16 ? 2 : 1); }
+__host__ __device__ constexpr int wrow_spl(int L) { return L <= 8 ? MPSP_WU : 1; }
 
 struct PartView {
   const int64_t* slice_ptr;   // [nslices+1] entry offsets (multiples of 32)
@@ -43,10 +43,8 @@ struct PartView {
   const uint32_t* limbs;      // [nentries * L]
   int64_t nslots;             // 32 * nslices (SELL part: short rows)
   int64_t nslices;
-  // warp rows (rows longer than the long-row threshold), longest first;
-  // the first npcrow of them (length >= the pc threshold) go to spmv_pcrow
+  // warp rows (rows longer than the long-row threshold), longest first
   int64_t nwrow;
-  int64_t npcrow;
   const int64_t* wrow_ptr;    // [nwrow] first entry (multiple of 32)
   const int32_t* wrow_row;    // [nwrow] output row (local)
   const int32_t* wrow_len;    // [nwrow]
@@ -82,10 +80,6 @@ int launch_spmv_long(int L, const PartView& P, const XView& x, const YView& y, v
                      bool dense = false);
 // Row-length threshold above which a row goes to the warp-row kernel.
 int long_row_threshold();
-// Row-length threshold from which a warp row goes to spmv_pcrow.
-int pc_row_threshold();
-// Producer/consumer kernel over warp rows [0, P.npcrow); cudaError_t value.
-int launch_spmv_pc(int L, const PartView& P, const XView& x, const YView& y, void* stream);
 // Launch counter increment (shared by the kernel files).
 void launch_counter_add(int64_t k);
 // BiCG building blocks (krylov.cu); each returns a cudaError_t value.

@@ -120,8 +120,11 @@ __device__ __forceinline__ void add3w(uint32_t& a0, uint32_t& a1, uint32_t& a2, 
 #ifndef MPSP_NCH
 #define MPSP_NCH 2
 #endif
+#ifndef MPSP_NCH8
+#define MPSP_NCH8 1
+#endif
 template <int L>
-struct MulChains { static constexpr int n = L >= 16 ? MPSP_NCH : 1; };
+struct MulChains { static constexpr int n = L >= 16 ? MPSP_NCH : (L >= 4 ? MPSP_NCH8 : 1); };
 
 // --------------------------------------------------------------------------
 // t = RN_p(a * x).  a, x: L-limb mantissas (zero allowed: result zero).
@@ -254,7 +257,19 @@ __device__ __forceinline__ void mp_mul(const uint32_t (&a)[L], int32_t ea, uint3
     const bool amb = ((w1 | w2) == 0u) | ((w1 == 0x07FFFFFFu) & (w2 == wmask));
     const bool zero = (a[L - 1] == 0u) | (x[L - 1] == 0u);
     uint32_t stk = 1u;
-    if (amb && !zero) {                              // rare: complete the product
+    // Exact short product: every omitted term a_i x_j (i + j < K0) has i, j
+    // < K0, so N = 0 when either operand's limbs 0 .. K0-1 are all zero
+    // (e.g. a power-of-two mantissa: C5's diagonal 4, exact-integer data) -
+    // then T is the exact product and no lower column is formed.
+    bool low0 = false;
+    if (amb && !zero) {
+      uint32_t ao = 0u, xo = 0u;
+#pragma unroll
+      for (int i = 0; i < K0; ++i) { ao |= a[i]; xo |= x[i]; }
+      low0 = (ao == 0u) | (xo == 0u);
+      if (low0) stk = T[0] | T[1] | ((T[2] << sh) << 1);
+    }
+    if (amb && !zero && !low0) {                     // rare: complete the product
       uint32_t c0, c1, c2;
       const uint32_t slo = comba_lower<L, K0>(a, x, c0, c1, c2);
       uint32_t C[L + 3];
@@ -368,7 +383,13 @@ __device__ __forceinline__ uint32_t add_n_cin(uint32_t (&z)[N], const uint32_t (
 template <int L>
 __device__ __forceinline__ void mp_add(MP<L>& s, const MP<L>& t) {
   const bool tz = t.is_zero(), sz = s.is_zero();
-  const uint32_t mlt = lt_n<L>(s.m, t.m);               // |M_s| < |M_t|
+  // |M_s| < |M_t| matters only for equal exponents: the top limbs decide it
+  // unless they are equal too (rare: then the full borrow chain, warp-uniform)
+  uint32_t mlt = s.m[L - 1] < t.m[L - 1] ? 1u : 0u;
+  if constexpr (L > 1) {
+    if (__any_sync(__activemask(), (t.e == s.e) & (s.m[L - 1] == t.m[L - 1])))
+      mlt = lt_n<L>(s.m, t.m);
+  }
   // bitwise (not short-circuit) logic: no branches in the common path
   const bool t_big = !tz & (sz | (t.e > s.e) | ((t.e == s.e) & (mlt != 0u)));
   const int32_t eb = t_big ? t.e : s.e;

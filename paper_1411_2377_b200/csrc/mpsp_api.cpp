@@ -52,7 +52,7 @@ void parallel_for(int64_t n, F f) {
 }
 
 struct DevPart {
-  int64_t nrows = 0, nnz = 0, nslices = 0, nentries = 0, nwrow = 0, npcrow = 0;
+  int64_t nrows = 0, nnz = 0, nslices = 0, nentries = 0, nwrow = 0;
   int32_t max_len = 0;
   int64_t* slice_ptr = nullptr;
   int32_t* slot_row = nullptr;
@@ -70,7 +70,7 @@ struct DevPart {
     v.slice_ptr = slice_ptr; v.slot_row = slot_row; v.slot_len = slot_len;
     v.col = col; v.expw = expw; v.limbs = limbs;
     v.nslices = nslices; v.nslots = nslices * 32;
-    v.nwrow = nwrow; v.npcrow = npcrow; v.wrow_ptr = wrow_ptr; v.wrow_row = wrow_row; v.wrow_len = wrow_len;
+    v.nwrow = nwrow; v.wrow_ptr = wrow_ptr; v.wrow_row = wrow_row; v.wrow_len = wrow_len;
     return v;
   }
   void release() {
@@ -95,8 +95,8 @@ struct mpsp_csr {
   mutable const void* ptr_ok[6] = {};   // x/y pointers of the last mpsp_spmv(_t) call that passed the checks
   DevPart A, T;
   // fork/join for running the long-row and short-row kernels concurrently
-  cudaStream_t aux = nullptr, aux2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // host-buffer API workspace (lazily allocated)
   cudaStream_t stream = nullptr;
   void* ws = nullptr;
@@ -141,12 +141,6 @@ int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32
   int64_t nw = 0;
   while (nw < nrows && lrp[order[(size_t)nw] + 1] - lrp[order[(size_t)nw]] > T) ++nw;
   P.nwrow = nw;
-  {
-    const int64_t Tpc = (wide || dense) ? INT64_MAX : std::max<int64_t>(pc_row_threshold(), T + 1);
-    int64_t np = 0;
-    while (np < nw && lrp[order[(size_t)np] + 1] - lrp[order[(size_t)np]] >= Tpc) ++np;
-    P.npcrow = np;
-  }
   std::vector<int64_t> wptr((size_t)nw);
   std::vector<int32_t> wrow((size_t)nw), wlen((size_t)nw);
   int64_t ew = 0;
@@ -155,7 +149,7 @@ int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32
     wptr[(size_t)i] = ew;
     wrow[(size_t)i] = r;
     wlen[(size_t)i] = (int32_t)(lrp[r + 1] - lrp[r]);
-    const int64_t cs = wide ? 1 : (i < P.npcrow ? 32 * pc_spl(L) : 32);
+    const int64_t cs = wide ? 1 : 32 * wrow_spl(L);
     ew += (wlen[(size_t)i] + cs - 1) / cs * cs;
   }
   // SELL slices of the remaining rows
@@ -211,8 +205,8 @@ int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32
   parallel_for(nw, [&](int64_t i0, int64_t i1) {
     for (int64_t i = i0; i < i1; ++i) {
       const int32_t r = wrow[(size_t)i];
-      if (i < P.npcrow) {                         // chunk-permuted (layout.h)
-        const int U = pc_spl(L);
+      if (!wide) {                                // chunk-permuted (layout.h)
+        const int U = wrow_spl(L);
         for (int64_t j = 0; j < wlen[(size_t)i]; ++j) {
           const int64_t c = j / (32 * U), q = j % (32 * U);
           put(wptr[(size_t)i] + c * 32 * U + 32 * (q % U) + q / U, lrp[r] + j);
@@ -351,30 +345,21 @@ int do_spmv(const mpsp_csr* A, bool transpose, const uint32_t* xl, const int32_t
                            : launch_spmv_long(L, pv, xv, yv, stream, true);
     return err ? cuda_fail((cudaError_t)err) : MPSP_OK;
   }
-  const bool has_pc = pv.npcrow > 0, has_w = pv.nwrow > pv.npcrow, has_s = pv.nslots > 0;
+  const bool has_w = pv.nwrow > 0, has_s = pv.nslots > 0;
   cudaStream_t us = (cudaStream_t)stream;
   cudaError_t ce;
   int err;
-  if ((int)has_pc + (int)has_w + (int)has_s > 1 && A->aux) {
-    // longest rows (critical path) on the high-priority aux stream, the other
-    // warp rows on aux2, short rows on the caller's stream; joined back there
+  if (has_w && has_s && A->aux) {
+    // warp rows (the longest rows: the critical path) on the high-priority
+    // aux stream, short rows on the caller's stream; joined back there
     if ((ce = cudaEventRecord(A->ev_fork, us)) != cudaSuccess) return cuda_fail(ce);
-    if (has_pc) {
-      if ((ce = cudaStreamWaitEvent(A->aux, A->ev_fork, 0)) != cudaSuccess) return cuda_fail(ce);
-      if ((err = launch_spmv_pc(L, pv, xv, yv, A->aux)) != 0) return cuda_fail((cudaError_t)err);
-      if ((ce = cudaEventRecord(A->ev_join, A->aux)) != cudaSuccess) return cuda_fail(ce);
-    }
-    if (has_w) {
-      if ((ce = cudaStreamWaitEvent(A->aux2, A->ev_fork, 0)) != cudaSuccess) return cuda_fail(ce);
-      if ((err = launch_spmv_long(L, pv, xv, yv, A->aux2)) != 0) return cuda_fail((cudaError_t)err);
-      if ((ce = cudaEventRecord(A->ev_join2, A->aux2)) != cudaSuccess) return cuda_fail(ce);
-    }
-    if (has_s && (err = launch_spmv(L, pv, xv, yv, stream)) != 0) return cuda_fail((cudaError_t)err);
-    if (has_pc && (ce = cudaStreamWaitEvent(us, A->ev_join, 0)) != cudaSuccess) return cuda_fail(ce);
-    if (has_w && (ce = cudaStreamWaitEvent(us, A->ev_join2, 0)) != cudaSuccess) return cuda_fail(ce);
+    if ((ce = cudaStreamWaitEvent(A->aux, A->ev_fork, 0)) != cudaSuccess) return cuda_fail(ce);
+    if ((err = launch_spmv_long(L, pv, xv, yv, A->aux)) != 0) return cuda_fail((cudaError_t)err);
+    if ((ce = cudaEventRecord(A->ev_join, A->aux)) != cudaSuccess) return cuda_fail(ce);
+    if ((err = launch_spmv(L, pv, xv, yv, stream)) != 0) return cuda_fail((cudaError_t)err);
+    if ((ce = cudaStreamWaitEvent(us, A->ev_join, 0)) != cudaSuccess) return cuda_fail(ce);
     return MPSP_OK;
   }
-  if ((err = launch_spmv_pc(L, pv, xv, yv, stream)) != 0) return cuda_fail((cudaError_t)err);
   if ((err = launch_spmv_long(L, pv, xv, yv, stream)) != 0) return cuda_fail((cudaError_t)err);
   if ((err = launch_spmv(L, pv, xv, yv, stream)) != 0) return cuda_fail((cudaError_t)err);
   return MPSP_OK;
@@ -534,10 +519,8 @@ static int create_impl(mpsp_csr** out, int p_bits, int64_t n, const int64_t* row
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
     if ((ce = cudaStreamCreateWithPriority(&H->aux, cudaStreamNonBlocking, prio_hi)) != cudaSuccess ||
-        (ce = cudaStreamCreateWithPriority(&H->aux2, cudaStreamNonBlocking, prio_hi)) != cudaSuccess ||
         (ce = cudaEventCreateWithFlags(&H->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
-        (ce = cudaEventCreateWithFlags(&H->ev_join, cudaEventDisableTiming)) != cudaSuccess ||
-        (ce = cudaEventCreateWithFlags(&H->ev_join2, cudaEventDisableTiming)) != cudaSuccess)
+        (ce = cudaEventCreateWithFlags(&H->ev_join, cudaEventDisableTiming)) != cudaSuccess)
       rc = cuda_fail(ce);
   }
   if (rc == MPSP_OK) {
@@ -563,10 +546,8 @@ void mpsp_destroy(mpsp_csr* A) {
   if (A->ws) cudaFree(A->ws);
   if (A->stream) cudaStreamDestroy(A->stream);
   if (A->aux) cudaStreamDestroy(A->aux);
-  if (A->aux2) cudaStreamDestroy(A->aux2);
   if (A->ev_fork) cudaEventDestroy(A->ev_fork);
   if (A->ev_join) cudaEventDestroy(A->ev_join);
-  if (A->ev_join2) cudaEventDestroy(A->ev_join2);
   cudaSetDevice(cur);
   cudaGetLastError();
   delete A;

@@ -203,7 +203,11 @@ template <int L>
 static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStream_t st) {
   const int64_t nshort = P.nslots;
   if (nshort <= 0) return 0;
-  const int threads = 128;
+  // threads per block (env MPSP_SELL_TPB, read per launch): smaller blocks
+  // spread few warps more evenly over the SMs
+  const char* vt = std::getenv("MPSP_SELL_TPB");
+  const int tpb = vt ? std::atoi(vt) : 128;
+  const int threads = (tpb == 32 || tpb == 64) ? tpb : 128;
   const int64_t blocks = (nshort + threads - 1) / threads;
   if constexpr (L == 32) {
     const char* vc = std::getenv("MPSP_CP");       // 0: register-prefetch kernel
@@ -227,7 +231,8 @@ static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStrea
   int minb = L == 16 ? 4 : 1;
   if (L <= 8) {
     const int sms = current_sms();
-    minb = (blocks > (int64_t)sms * 5 && blocks <= (int64_t)sms * 6) ? 6 : 5;
+    const int64_t b128 = (nshort + 127) / 128;
+    minb = (b128 > (int64_t)sms * 5 && b128 <= (int64_t)sms * 6) ? 6 : 5;
   }
   if (vm) minb = std::atoi(vm);
   const unsigned nb = (unsigned)blocks;

@@ -194,154 +194,265 @@ struct WChain {
       // ---- the first failing step f
       const int f = __ffs(failM) - 1;
       if (lane < f) add_n<N>(R, R, Q);               // steps before f are valid
-      // One-binade transitions (tests/test_kernel_algorithms.py models them):
-      // if step f's exact sum V = S + tau provably crosses 2^p (equal signs)
-      // or provably lands in [2^(p-2), 2^(p-1)) (opposite signs), it is
-      // rounded directly on the new grid 2u / u/2 from the low bits of
-      // W = S (+ floor tau) - read off the lanes' R by ballots - and tau's
-      // fraction bits; R is halved / doubled lane by lane.  Everything else
-      // takes the exact path below.
-      {
-        const uint32_t fy = Y[0];                     // tau's 32 fraction bits
-        const bool fnz = (fy != 0u) || (stk != 0u);   // fraction != 0
-        const bool up_f = use && t.s == sg && LB + h - 1 >= HI;
-        const bool dn_f = use && t.s != sg && LB + ek + h + 2 <= LO && LB + h - 1 >= LO / 2;
-        // dominant product (|t| >= 2^(E-1), t.e - E = dd in [0, 27]): the binade
-        // E + k of V = S u + t certified from the high-part bounds and t's top
-        // 32 bits (units 2^(E-HB)); t/u = M_t 2^dd is an integer
-        const int dd = (int)min(max(-d64, (int64_t)0), (int64_t)27);
-        const uint32_t mt = t.m[L - 1];
-        const int64_t tl = dd >= 6 ? ((int64_t)mt << (dd - 6)) : (int64_t)(mt >> (6 - dd));
-        const int64_t th = tl + (dd >= 6 ? ((int64_t)1 << (dd - 6)) : (int64_t)1);
-        const bool same = t.s == sg;
-        const int64_t vlo = same ? (int64_t)LB + tl : tl - (int64_t)LB - ek;
-        const int64_t vhi = same ? (int64_t)LB + ek + th : th - (int64_t)LB + 1;
-        const int kd = vlo > 0 ? (64 - __clzll(vlo)) - HB : 0;
-        const bool dom_f = badd && -d64 <= 27 && kd >= 1 && kd <= 26 &&
-                           vhi <= ((int64_t)1 << (HB + kd)) - 1;
-#ifdef MPSP_TRANS_MASK
-        const int mode = __shfl_sync(FULL, up_f ? 1 : (dn_f ? 2 : (dom_f ? 4 : 0)), f) & MPSP_TRANS_MASK;
-#else
-        const int mode = __shfl_sync(FULL, up_f ? 1 : (dn_f ? 2 : (dom_f ? 4 : 0)), f);
-#endif
-        if (mode == 4) {
-          const int k = __shfl_sync(FULL, kd, f);
-          const int64_t vlof = __shfl_sync(FULL, vlo, f), vhif = __shfl_sync(FULL, vhi, f);
-          const uint32_t sgf = __shfl_sync(FULL, t.s, f);
-          if (sgf != sg) {                            // S := -S: W = |t|/u - S > 0
-#pragma unroll
-            for (int i = 0; i < N; ++i) R[i] = ~R[i];
-            inc_n<N>(R, 1u);
-          }
-          if (lane == f) {                            // W = R-sum + M_t << dd
-            uint32_t Yv[N];
-            Yv[0] = t.m[0] << dd;
-#pragma unroll
-            for (int i = 1; i < L; ++i) Yv[i] = __funnelshift_l(t.m[i - 1], t.m[i], dd);
-            Yv[L] = dd ? (t.m[L - 1] >> (32 - dd)) : 0u;
-            Yv[L + 1] = 0u;
-            add_n<N>(R, R, Yv);
-          }
-          // RN_int(W / 2^k): W mod 2^k from the lanes' low k bits (k <= 26:
-          // their sum fits 31 bits), floor(W / 2^k) = sum of the lanes'
-          // arithmetic shifts + the carry of that sum
-          const uint32_t lows = __reduce_add_sync(FULL, R[0] & ((1u << k) - 1u));
-          const uint32_t c = lows >> k;
-          const uint32_t rb = (lows >> (k - 1)) & 1u;
-          const uint32_t stk2 = (lows & ((1u << (k - 1)) - 1u)) != 0u ? 1u : 0u;
-          const uint32_t par = ((uint32_t)__popc(__ballot_sync(FULL, (R[0] >> k) & 1u)) + c) & 1u;
-          const uint32_t incr = rb & (stk2 | par);
-#pragma unroll
-          for (int i = 0; i < N - 1; ++i) R[i] = __funnelshift_r(R[i], R[i + 1], k);
-          R[N - 1] = (uint32_t)((int32_t)R[N - 1] >> k);
-          if (lane == 0) {
-            uint32_t Cv[N];
-            Cv[0] = c + incr;
-#pragma unroll
-            for (int i = 1; i < N; ++i) Cv[i] = 0u;
-            add_n<N>(R, R, Cv);
-          }
-          sg = sgf;
-          E += k;
-          Shi = (int32_t)((vlof >> k) - 1);
-          err = (int32_t)((vhif >> k) - (vlof >> k) + 3);
-          start = f + 1;
-          continue;
-        }
-        if (mode != 0) {
-          const int32_t LBf = __shfl_sync(FULL, LB, f);
-          const int32_t hf = __shfl_sync(FULL, h, f);
-          const int32_t ekf = __shfl_sync(FULL, ek, f);
-          if (mode == 1) {                            // V in [2^p, 1.5 2^p): grid 2u
-            if (lane == f) {
-              uint32_t Yv[N];
-#pragma unroll
-              for (int i = 0; i < L; ++i) Yv[i] = Y[i + 1];
-              Yv[L] = 0u;
-              Yv[L + 1] = 0u;
-              add_n<N>(R, R, Yv);                     // W = S + floor(tau)
-            }
-            const uint32_t c0 = (uint32_t)__popc(__ballot_sync(FULL, R[0] & 1u));
-            const uint32_t c1 = (uint32_t)__popc(__ballot_sync(FULL, (R[0] >> 1) & 1u));
-            const uint32_t w0 = c0 & 1u, w1 = ((c0 >> 1) + c1) & 1u;
-            const uint32_t frac = __shfl_sync(FULL, fnz ? 1u : 0u, f);
-            const uint32_t incr = w0 & (frac | w1);   // RNE of W/2 + (w0 + frac)/2
-#pragma unroll
-            for (int i = 0; i < N - 1; ++i) R[i] = __funnelshift_r(R[i], R[i + 1], 1);
-            R[N - 1] = (uint32_t)((int32_t)R[N - 1] >> 1);
-            if (lane == 0) {
-              uint32_t Cv[N];
-              Cv[0] = (c0 >> 1) + incr;
-#pragma unroll
-              for (int i = 1; i < N; ++i) Cv[i] = 0u;
-              add_n<N>(R, R, Cv);                     // sum of halves + lost carries
-            }
-            E += 1;
-            Shi = (LBf + hf - 1) >> 1;
-            err = ((ekf + 3) >> 1) + 2;
-          } else {                                    // V in [2^(p-2), 2^(p-1)): grid u/2
-#pragma unroll
-            for (int i = N - 1; i > 0; --i) R[i] = __funnelshift_l(R[i - 1], R[i], 1);
-            R[0] <<= 1;
-            const uint32_t b1 = fy >> 31, b2 = (fy >> 30) & 1u;
-            const bool low = ((fy << 1) != 0u) || (stk != 0u);
-            const bool tie2 = b2 && ((fy << 2) == 0u) && (stk == 0u);
-            if (lane == f) {                          // R -= 2 floor(tau) + b1 (+1 if low)
-              uint32_t Yv[N];                         // (floor(tau) << 1) | b1
-#pragma unroll
-              for (int i = 0; i < N; ++i) {
-                const uint32_t lo_ = (i >= 1 && i - 1 < L) ? Y[i] : 0u;      // limb i-1
-                const uint32_t cur = (i < L) ? Y[i + 1] : 0u;                // limb i
-                Yv[i] = __funnelshift_l(lo_, cur, 1);
-              }
-              Yv[0] |= b1;
-              sub_n<N>(R, R, Yv, low ? 1u : 0u);
-            }
-            const uint32_t low_f = __shfl_sync(FULL, low ? 1u : 0u, f);
-            const uint32_t b1f = __shfl_sync(FULL, b1, f), b2f = __shfl_sync(FULL, b2, f);
-            const uint32_t tie2f = __shfl_sync(FULL, tie2 ? 1u : 0u, f);
-            if (lane == 0 && low_f) {
-              const uint32_t upb = (b2f == 0u) | (tie2f & (b1f ^ 1u));
-              inc_n<N>(R, upb);
-            }
-            E -= 1;
-            Shi = 2 * (LBf + hf - 1) - 2;
-            err = 2 * (ekf + 2) + 4;
-          }
-          start = f + 1;
-          continue;
-        }
-      }
-      MP<L> s, tf;
-      exact(s);
-#pragma unroll
-      for (int i = 0; i < L; ++i) tf.m[i] = __shfl_sync(FULL, t.m[i], f);
-      tf.e = __shfl_sync(FULL, t.e, f);
-      tf.s = __shfl_sync(FULL, t.s, f);
-      mp_add<L>(s, tf);
-      reset_to(s, lane);
+      step_f(t, f, __shfl_sync(FULL, LB, f), __shfl_sync(FULL, h, f), err + f, lane);
       start = f + 1;
     }
+  }
+
+  // The first failing step f of a block: lane f holds its product t; LBf, hf,
+  // ekf are its high-part bounds (S_{f-1}/H in [LBf, LBf + ekf), h_f =
+  // floor(Q_f / H)).  One-binade transitions (tests/test_kernel_algorithms.py
+  // models them): if step f's exact sum V = S + tau provably crosses 2^p
+  // (equal signs) or provably lands in [2^(p-2), 2^(p-1)) (opposite signs),
+  // it is rounded directly on the new grid 2u / u/2 from the low bits of
+  // W = S (+ floor tau) - read off the lanes' R by ballots - and tau's
+  // fraction bits; R is halved / doubled lane by lane.  A dominant product
+  // (|t| >= 2^(E-1)) whose sum's binade E + k is certified is rounded on the
+  // grid 2^k u from one redux over the lanes' R.  Everything else takes the
+  // exact adder.  All lanes call it (warp-uniform control flow).
+  __device__ __forceinline__ void step_f(const MP<L>& t, int f, int32_t LBf, int32_t hf,
+                                         int32_t ekf, int lane) {
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int32_t LO = 1 << (HB - 1), HI = 1 << HB;
+    const bool act = !t.is_zero();
+    const int64_t d64 = (int64_t)E - (int64_t)t.e;
+    const bool badd = act && d64 < 1;                // |t| >= 2^(E-1)
+    const bool use = act && !badd;
+    const uint32_t dd0 = use ? (uint32_t)min(d64, (int64_t)(32 * L + 32)) : 0u;
+    uint32_t Y[L + 1];
+    Y[0] = 0u;
+#pragma unroll
+    for (int i = 0; i < L; ++i) Y[i + 1] = t.m[i];
+    uint32_t stk = 0u;
+    shr_bits_sticky<L + 1>(Y, dd0, stk);
+    {
+      const uint32_t fy = Y[0];                     // tau's 32 fraction bits
+      const bool fnz = (fy != 0u) || (stk != 0u);   // fraction != 0
+      const bool up_f = use && t.s == sg && LBf + hf - 1 >= HI;
+      const bool dn_f = use && t.s != sg && LBf + ekf + hf + 2 <= LO && LBf + hf - 1 >= LO / 2;
+      // dominant product (|t| >= 2^(E-1), t.e - E = dd in [0, 27]): the binade
+      // E + k of V = S u + t certified from the high-part bounds and t's top
+      // 32 bits (units 2^(E-HB)); t/u = M_t 2^dd is an integer
+      const int dd = (int)min(max(-d64, (int64_t)0), (int64_t)27);
+      const uint32_t mt = t.m[L - 1];
+      const int64_t tl = dd >= 6 ? ((int64_t)mt << (dd - 6)) : (int64_t)(mt >> (6 - dd));
+      const int64_t th = tl + (dd >= 6 ? ((int64_t)1 << (dd - 6)) : (int64_t)1);
+      const bool same = t.s == sg;
+      const int64_t vlo = same ? (int64_t)LBf + tl : tl - (int64_t)LBf - ekf;
+      const int64_t vhi = same ? (int64_t)LBf + ekf + th : th - (int64_t)LBf + 1;
+      const int kd = vlo > 0 ? (64 - __clzll(vlo)) - HB : 0;
+      const bool dom_f = badd && -d64 <= 27 && kd >= 1 && kd <= 26 &&
+                         vhi <= ((int64_t)1 << (HB + kd)) - 1;
+#ifdef MPSP_TRANS_MASK
+      const int mode = __shfl_sync(FULL, up_f ? 1 : (dn_f ? 2 : (dom_f ? 4 : 0)), f) & MPSP_TRANS_MASK;
+#else
+      const int mode = __shfl_sync(FULL, up_f ? 1 : (dn_f ? 2 : (dom_f ? 4 : 0)), f);
+#endif
+      if (mode == 4) {
+        const int k = __shfl_sync(FULL, kd, f);
+        const int64_t vlof = __shfl_sync(FULL, vlo, f), vhif = __shfl_sync(FULL, vhi, f);
+        const uint32_t sgf = __shfl_sync(FULL, t.s, f);
+        if (sgf != sg) {                            // S := -S: W = |t|/u - S > 0
+#pragma unroll
+          for (int i = 0; i < N; ++i) R[i] = ~R[i];
+          inc_n<N>(R, 1u);
+        }
+        if (lane == f) {                            // W = R-sum + M_t << dd
+          uint32_t Yv[N];
+          Yv[0] = t.m[0] << dd;
+#pragma unroll
+          for (int i = 1; i < L; ++i) Yv[i] = __funnelshift_l(t.m[i - 1], t.m[i], dd);
+          Yv[L] = dd ? (t.m[L - 1] >> (32 - dd)) : 0u;
+          Yv[L + 1] = 0u;
+          add_n<N>(R, R, Yv);
+        }
+        // RN_int(W / 2^k): W mod 2^k from the lanes' low k bits (k <= 26:
+        // their sum fits 31 bits), floor(W / 2^k) = sum of the lanes'
+        // arithmetic shifts + the carry of that sum
+        const uint32_t lows = __reduce_add_sync(FULL, R[0] & ((1u << k) - 1u));
+        const uint32_t c = lows >> k;
+        const uint32_t rb = (lows >> (k - 1)) & 1u;
+        const uint32_t stk2 = (lows & ((1u << (k - 1)) - 1u)) != 0u ? 1u : 0u;
+        const uint32_t par = ((uint32_t)__popc(__ballot_sync(FULL, (R[0] >> k) & 1u)) + c) & 1u;
+        const uint32_t incr = rb & (stk2 | par);
+#pragma unroll
+        for (int i = 0; i < N - 1; ++i) R[i] = __funnelshift_r(R[i], R[i + 1], k);
+        R[N - 1] = (uint32_t)((int32_t)R[N - 1] >> k);
+        if (lane == 0) {
+          uint32_t Cv[N];
+          Cv[0] = c + incr;
+#pragma unroll
+          for (int i = 1; i < N; ++i) Cv[i] = 0u;
+          add_n<N>(R, R, Cv);
+        }
+        sg = sgf;
+        E += k;
+        Shi = (int32_t)((vlof >> k) - 1);
+        err = (int32_t)((vhif >> k) - (vlof >> k) + 3);
+        return;
+      }
+      if (mode == 1) {                              // V in [2^p, 1.5 2^p): grid 2u
+        if (lane == f) {
+          uint32_t Yv[N];
+#pragma unroll
+          for (int i = 0; i < L; ++i) Yv[i] = Y[i + 1];
+          Yv[L] = 0u;
+          Yv[L + 1] = 0u;
+          add_n<N>(R, R, Yv);                       // W = S + floor(tau)
+        }
+        const uint32_t c0 = (uint32_t)__popc(__ballot_sync(FULL, R[0] & 1u));
+        const uint32_t c1 = (uint32_t)__popc(__ballot_sync(FULL, (R[0] >> 1) & 1u));
+        const uint32_t w0 = c0 & 1u, w1 = ((c0 >> 1) + c1) & 1u;
+        const uint32_t frac = __shfl_sync(FULL, fnz ? 1u : 0u, f);
+        const uint32_t incr = w0 & (frac | w1);     // RNE of W/2 + (w0 + frac)/2
+#pragma unroll
+        for (int i = 0; i < N - 1; ++i) R[i] = __funnelshift_r(R[i], R[i + 1], 1);
+        R[N - 1] = (uint32_t)((int32_t)R[N - 1] >> 1);
+        if (lane == 0) {
+          uint32_t Cv[N];
+          Cv[0] = (c0 >> 1) + incr;
+#pragma unroll
+          for (int i = 1; i < N; ++i) Cv[i] = 0u;
+          add_n<N>(R, R, Cv);                       // sum of halves + lost carries
+        }
+        E += 1;
+        Shi = (LBf + hf - 1) >> 1;
+        err = ((ekf + 3) >> 1) + 2;
+        return;
+      }
+      if (mode == 2) {                              // V in [2^(p-2), 2^(p-1)): grid u/2
+#pragma unroll
+        for (int i = N - 1; i > 0; --i) R[i] = __funnelshift_l(R[i - 1], R[i], 1);
+        R[0] <<= 1;
+        const uint32_t b1 = fy >> 31, b2 = (fy >> 30) & 1u;
+        const bool low = ((fy << 1) != 0u) || (stk != 0u);
+        const bool tie2 = b2 && ((fy << 2) == 0u) && (stk == 0u);
+        if (lane == f) {                            // R -= 2 floor(tau) + b1 (+1 if low)
+          uint32_t Yv[N];                           // (floor(tau) << 1) | b1
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            const uint32_t lo_ = (i >= 1 && i - 1 < L) ? Y[i] : 0u;      // limb i-1
+            const uint32_t cur = (i < L) ? Y[i + 1] : 0u;                // limb i
+            Yv[i] = __funnelshift_l(lo_, cur, 1);
+          }
+          Yv[0] |= b1;
+          sub_n<N>(R, R, Yv, low ? 1u : 0u);
+        }
+        const uint32_t low_f = __shfl_sync(FULL, low ? 1u : 0u, f);
+        const uint32_t b1f = __shfl_sync(FULL, b1, f), b2f = __shfl_sync(FULL, b2, f);
+        const uint32_t tie2f = __shfl_sync(FULL, tie2 ? 1u : 0u, f);
+        if (lane == 0 && low_f) {
+          const uint32_t upb = (b2f == 0u) | (tie2f & (b1f ^ 1u));
+          inc_n<N>(R, upb);
+        }
+        E -= 1;
+        Shi = 2 * (LBf + hf - 1) - 2;
+        err = 2 * (ekf + 2) + 4;
+        return;
+      }
+    }
+    MP<L> s, tf;
+    exact(s);
+#pragma unroll
+    for (int i = 0; i < L; ++i) tf.m[i] = __shfl_sync(FULL, t.m[i], f);
+    tf.e = __shfl_sync(FULL, t.e, f);
+    tf.s = __shfl_sync(FULL, t.s, f);
+    mp_add<L>(s, tf);
+    reset_to(s, lane);
+  }
+
+  // s := the chain over this warp's 32U products, lane k holding the U
+  // consecutive steps Uk .. Uk+U-1 in t[0..U-1] (zero limbs: no step).  One
+  // warp scan and one ballot per 32U steps; the U alignments of a lane are
+  // independent.  A grid tie is sent to step_f (exact path) instead of being
+  // resolved from the running parity (rare on the configs; the stress corpus
+  // forces it).
+  template <int U>
+  __device__ __forceinline__ void consume_u(const MP<L> (&t)[U], int lane) {
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int32_t LO = 1 << (HB - 1), HI = 1 << HB;
+    constexpr int CS = 32 * U;
+    bool tz[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) tz[u] = t[u].is_zero();
+    int start = 0;
+    while (start < CS) {
+      if (szero) {
+        int fu = U;
+#pragma unroll
+        for (int u = U - 1; u >= 0; --u)
+          if (!tz[u] && U * lane + u >= start) fu = u;
+        const unsigned nzm = __ballot_sync(FULL, fu < U);
+        if (nzm == 0u) break;
+        const int kf = __ffs(nzm) - 1;
+        const int uf = __shfl_sync(FULL, fu, kf);
+        MP<L> tf;
+        pick<U>(t, uf, tf);
+#pragma unroll
+        for (int i = 0; i < L; ++i) tf.m[i] = __shfl_sync(FULL, tf.m[i], kf);
+        tf.e = __shfl_sync(FULL, tf.e, kf);
+        tf.s = __shfl_sync(FULL, tf.s, kf);
+        reset_to(tf, lane);
+        start = U * kf + uf + 1;
+        continue;
+      }
+      uint32_t Q[U][N];
+      int32_t h[U], Hx[U];
+      bool bad[U];
+      int32_t tot = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool act = (U * lane + u >= start) && !tz[u];
+        align_q<L>(t[u], act, E, sg, Q[u], h[u], bad[u]);
+        Hx[u] = tot;
+        tot += h[u];
+      }
+      int32_t Pi = tot;                               // inclusive scan of the lane totals
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t v = __shfl_up_sync(FULL, Pi, o);
+        if (lane >= o) Pi += v;
+      }
+      const int32_t X = Shi + Pi - tot;               // S/H before this lane's first step >= X
+      int fu = U;
+#pragma unroll
+      for (int u = U - 1; u >= 0; --u) {
+        const bool act = (U * lane + u >= start) && !tz[u];
+        const int32_t LB = X + Hx[u];
+        const int32_t ek = err + U * lane + u;
+        const bool ok = !act || (!bad[u] && LB + h[u] - 1 >= LO && LB + ek + h[u] + 1 <= HI);
+        if (!ok) fu = u;
+      }
+      const unsigned failM = __ballot_sync(FULL, fu < U);
+      if (failM == 0u) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) add_n<N>(R, R, Q[u]);
+        Shi += __shfl_sync(FULL, Pi, 31);
+        err = min(err + CS, 1 << 28);                 // saturates: checks then fail
+        break;
+      }
+      const int kf = __ffs(failM) - 1;
+      const int uf = __shfl_sync(FULL, fu, kf);
+      int32_t LBl = 0, hl = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (lane < kf || (lane == kf && u < uf)) add_n<N>(R, R, Q[u]);   // steps before f
+        if (u == uf) { LBl = X + Hx[u]; hl = h[u]; }
+      }
+      MP<L> tu;
+      pick<U>(t, uf, tu);
+      step_f(tu, kf, __shfl_sync(FULL, LBl, kf), __shfl_sync(FULL, hl, kf), err + U * kf + uf, lane);
+      start = U * kf + uf + 1;
+    }
+  }
+
+  // t[uf] for a warp-uniform runtime index uf (no dynamic register indexing)
+  template <int U>
+  __device__ __forceinline__ static void pick(const MP<L> (&t)[U], int uf, MP<L>& o) {
+    o = t[0];
+#pragma unroll
+    for (int u = 1; u < U; ++u)
+      if (u == uf) o = t[u];
   }
 };
 

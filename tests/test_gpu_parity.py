@@ -160,28 +160,29 @@ def test_tie_prone_rows(p, thr, monkeypatch):
 
 
 @pytest.fixture
-def all_rows_pc(monkeypatch):
-    """Route every nonempty row through the producer/consumer kernel."""
+def all_rows_warp(monkeypatch):
+    """Route every nonempty row through the warp-row kernel (U steps per lane,
+    layout.h wrow_spl: chunks of 64 steps at p <= 256, 32 above)."""
     monkeypatch.setenv("MPSP_LONG_T", "0")
-    monkeypatch.setenv("MPSP_PC_T", "1")
 
 
 @pytest.mark.parametrize("p", PS)
-def test_pc_kernel_stress(p, all_rows_pc):
+def test_warp_kernel_stress(p, all_rows_warp):
     d = gen.stress(p, seed=9)
     for op in ("ax", "atx"):
-        assert_same(gpu_run(d, op), oracle_full(d, op), f"pc-kernel stress p={p} {op}")
+        assert_same(gpu_run(d, op), oracle_full(d, op), f"warp-row stress p={p} {op}")
 
 
 @pytest.mark.parametrize("p", [32, 256, 1024])
-def test_pc_kernel_tie_prone(p, all_rows_pc):
+def test_warp_kernel_tie_prone(p, all_rows_warp):
     d = _tie_prone_rows(p, 60, seed=p + 5)
-    assert_same(gpu_run(d, "ax"), oracle_full(d, "ax"), f"pc tie-prone p={p}")
+    assert_same(gpu_run(d, "ax"), oracle_full(d, "ax"), f"warp-row tie-prone p={p}")
 
 
-@pytest.mark.parametrize("pc", ["100", "300"])
-def test_pc_threshold_split_c4(pc, monkeypatch):
-    monkeypatch.setenv("MPSP_PC_T", pc)
+@pytest.mark.parametrize("thr", ["0", "31", "63", "100", "300"])
+def test_warp_threshold_split_c4(thr, monkeypatch):
+    """Row lengths around the 32- and 64-step chunk boundaries, ragged tails."""
+    monkeypatch.setenv("MPSP_LONG_T", thr)
     d = gen.make("C4", n=20_000, seed=10)
     for op in ("ax", "atx"):
-        assert_same(gpu_run(d, op), oracle_full(d, op), f"C4 pc threshold {pc} {op}")
+        assert_same(gpu_run(d, op), oracle_full(d, op), f"C4 warp threshold {thr} {op}")

@@ -111,8 +111,9 @@ HB = 26
 
 def block_sum_chain(ts, p, G=32, ties_exact=False, transitions=False, stats=None):
     """Model of spmv_wrow's chain over the products ts (oracle triples),
-    G steps per block.  ties_exact=True models spmv_pcrow's chain warp, which
-    sends a grid tie through the exact path instead of resolving its parity.
+    G steps per block.  ties_exact=True models WChain::consume_u (spmv_wrow,
+    G = 32U steps per warp pass), which sends a grid tie through the exact path
+    instead of resolving its parity.
     transitions=True models WChain's one-binade transitions: a failing step
     whose exact sum provably crosses 2^p (same signs) or provably drops to
     [2^(p-2), 2^(p-1)) (opposite signs) is rounded on the new grid directly
@@ -374,6 +375,10 @@ def test_block_sum_transitions_adversarial(p):
                 ts.append(_rand_t(rng, p, s_e - 3, s_e + 1))
         got, _ = block_sum_chain(ts, p, G=rng.choice([4, 32]), transitions=True)
         assert got == oracle_chain(ts, p), trial
+        # spmv_wrow's consume_u (64 steps per warp pass, grid ties sent to the
+        # exact path, transitions on)
+        got, _ = block_sum_chain(ts, p, G=64, transitions=True, ties_exact=True)
+        assert got == oracle_chain(ts, p), ("U=2", trial)
 
 
 @pytest.mark.parametrize("p", [32, 64, 256])
@@ -409,6 +414,8 @@ def test_block_sum_dominant_transitions(p):
             ts.append(_rand_t(rng, p, -40, 40))
         got, _ = block_sum_chain(ts, p, G=rng.choice([4, 32]), transitions=True, stats=st)
         assert got == oracle_chain(ts, p), trial
+        got, _ = block_sum_chain(ts, p, G=64, transitions=True, ties_exact=True)
+        assert got == oracle_chain(ts, p), ("U=2", trial)
     assert st.get("dom", 0) > 0
     # C4-like rows (products of values with exponents U[-32, 32]): the
     # dominant transition takes most of what used to be exact-path steps
@@ -419,3 +426,39 @@ def test_block_sum_dominant_transitions(p):
         got, _ = block_sum_chain(ts, p, transitions=True, stats=st)
         assert got == oracle_chain(ts, p), ("c4-like", trial)
     assert st.get("dom", 0) > 2 * st.get("exact", 0)
+
+
+@pytest.mark.parametrize("p", [128, 256, 1024])
+def test_short_product_zero_low_limbs_is_exact(p):
+    """mp_mul's exact case: when either operand's limbs 0 .. K0-1 (K0 = L-3)
+    are all zero, every omitted Comba term a_i x_j (i + j < K0) is zero, so
+    the upper columns T are the exact product and rounding T directly (round
+    bit and sticky read from T) equals RN(a*x) - e.g. C5's diagonal 4
+    (M = 2^(p-1)), whose products the certificate cannot decide (all-zero
+    bits below the round bit)."""
+    L = p // 32
+    K0 = L - 3
+    rng = random.Random(p + 99)
+    for _ in range(400):
+        hi_bits = 32 * (L - K0)
+        Ma = ((1 << (hi_bits - 1)) | rng.getrandbits(hi_bits - 1)) << (32 * K0)
+        if rng.random() < 0.3:
+            Ma = 1 << (p - 1)
+        Mx = (1 << (p - 1)) | rng.getrandbits(p - 1)
+        if rng.random() < 0.5:
+            Ma, Mx = Mx, Ma
+        a = [(Ma >> (32 * i)) & M32 for i in range(L)]
+        x = [(Mx >> (32 * i)) & M32 for i in range(L)]
+        T = sum(a[i] * x[j] << (32 * (i + j)) for i in range(L) for j in range(L) if i + j >= K0)
+        assert T == Ma * Mx
+        sh = 0 if (T >> (2 * p - 1)) & 1 else 1
+        q = T >> (p - sh)
+        rb = (T >> (p - sh - 1)) & 1
+        sticky = (T & ((1 << (p - sh - 1)) - 1)) != 0
+        q += rb & (1 if sticky else (q & 1))
+        dE = -sh
+        if q == 1 << p:
+            q >>= 1
+            dE += 1
+        s, M, E = oracle.mul((0, Ma, 0), (0, Mx, 0), p)
+        assert (M, E) == (q, dE)

@@ -14,7 +14,7 @@ for c in $CFGS; do
   cfg=${c%%:*}; op=ax; [[ "$c" == *:atx ]] && op=atx
   for combo in "${combos[@]}"; do
     log=gpurun_out/sweep_${TAG}.log
-    env $combo timeout 300 python bench.py --config $cfg --op $op --steps 10 --warmup 3 --no-cpu --no-e2e > $log 2>&1
+    env $combo timeout 300 python bench.py --config $cfg --op $op --steps 10 --warmup 3 --no-cpu --no-e2e --no-per-config > $log 2>&1
     echo "$c [$combo ] $(python -c "import json; d=json.loads(open('$log').read().strip().splitlines()[-1]); r=d['roofline']; print('kern_ms=%.4f frac=%.3f' % (r['kernel_ms'], r['frac_of_t_roof']))" 2>&1 | tail -1)"
   done
 done
