@@ -199,6 +199,98 @@ __global__ void __launch_bounds__(CP_THREADS, CpMinB<L>::v) spmv_sell_cp(PartVie
   store_y<L>(y, row, s);
 }
 
+// spmv_sell_cp1<L>: the same with ONE stage per operand (12 KB of shared
+// memory per warp instead of 16: 4 blocks of 128 threads fit an SM): entry
+// j+1's copies are issued once entry j's product has consumed the slots (the
+// thread's own slots: no write-after-read hazard), so they overlap the add of
+// entry j and the other warps' work; the accumulator is parked in its own
+// region during the product.
+template <int L, int MINB>
+__global__ void __launch_bounds__(CP_THREADS, MINB) spmv_sell_cp1(PartView P, XView x, YView y) {
+  constexpr int NC = L / 4;
+  extern __shared__ uint4 smc[];                 // [a|x|s][NC][thread]
+  const int tid = threadIdx.x;
+  const int64_t slot = (int64_t)blockIdx.x * blockDim.x + tid;
+  const bool live = slot < P.nslots;
+  const int row = live ? P.slot_row[slot] : -1;
+  if (row < 0) return;
+  const int len = P.slot_len[slot];
+  const int l = (int)(slot & 31);
+  const int64_t g0 = P.slice_ptr[slot >> 5] >> 5;
+  const int32_t* colp = P.col + g0 * 32 + l;
+  const int32_t* expp = P.expw + g0 * 32 + l;
+  const uint4* A4 = reinterpret_cast<const uint4*>(P.limbs);
+  const uint4* X4 = reinterpret_cast<const uint4*>(x.limbs);
+  auto sa = [&](int c) { return smc + (0 * NC + c) * CP_THREADS + tid; };
+  auto sx = [&](int c) { return smc + (1 * NC + c) * CP_THREADS + tid; };
+  auto ss = [&](int c) { return smc + (2 * NC + c) * CP_THREADS + tid; };
+  int32_t wq = 0, exq = 0;
+  uint32_t sq = 0u;
+  auto issue = [&](int j, int col) {
+    const uint4* ga = A4 + (g0 + j) * NC * 32 + l;
+    const uint4* gx = X4 + (int64_t)col * NC;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      cp_async16(sa(c), ga + c * 32);
+      cp_async16(sx(c), gx + c);
+    }
+    cp_async_commit();
+  };
+  MP<L> s;
+  s.set_zero();
+  int cn = 0, cn2 = 0;                           // columns of entries j+1, j+2
+  if (len > 0) {
+    const int c0 = __ldg(colp);
+    issue(0, c0);
+    wq = __ldg(expp);
+    exq = __ldg(x.exps + c0);
+    sq = __ldg(x.signs + c0);
+    if (len > 1) cn = __ldg(colp + 32);
+    if (len > 2) cn2 = __ldg(colp + 64);
+  }
+  for (int j = 0; j < len; ++j) {
+    // scalars of entry j+1 (registers, loaded a step ahead)
+    int32_t wn = 0, exn = 0;
+    uint32_t sn = 0u;
+    if (j + 1 < len) {
+      wn = __ldg(expp + 32 * (j + 1));
+      exn = __ldg(x.exps + cn);
+      sn = __ldg(x.signs + cn);
+    }
+    cp_async_wait<0>();                          // entry j has landed
+    uint32_t a[L], xv[L];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const uint4 va = *sa(c), vx = *sx(c);
+      a[4 * c] = va.x; a[4 * c + 1] = va.y; a[4 * c + 2] = va.z; a[4 * c + 3] = va.w;
+      xv[4 * c] = vx.x; xv[4 * c + 1] = vx.y; xv[4 * c + 2] = vx.z; xv[4 * c + 3] = vx.w;
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      *ss(c) = make_uint4(s.m[4 * c], s.m[4 * c + 1], s.m[4 * c + 2], s.m[4 * c + 3]);
+    MP<L> t;
+    const int32_t ea = (int32_t)((uint32_t)wq << 1) >> 1;
+    mp_mul<L>(a, ea, (uint32_t)wq >> 31, xv, exq, sq, t);
+    if (j + 1 < len) {                           // the slots are consumed: refill
+      issue(j + 1, cn);
+      cn = cn2;
+      if (j + 3 < len) cn2 = __ldg(colp + 32 * (j + 3));
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const uint4 v = *ss(c);
+      s.m[4 * c] = v.x; s.m[4 * c + 1] = v.y; s.m[4 * c + 2] = v.z; s.m[4 * c + 3] = v.w;
+    }
+    if (j == 0) {
+      s = t;                                     // RN(+0 + t) = t
+    } else {
+      mp_add<L>(s, t);
+    }
+    wq = wn; exq = exn; sq = sn;
+  }
+  store_y<L>(y, row, s);
+}
+
 template <int L>
 static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStream_t st) {
   const int64_t nshort = P.nslots;
@@ -210,13 +302,45 @@ static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStrea
   const int threads = (tpb == 32 || tpb == 64) ? tpb : 128;
   const int64_t blocks = (nshort + threads - 1) / threads;
   if constexpr (L == 32) {
-    const char* vc = std::getenv("MPSP_CP");       // 0: register-prefetch kernel
+    const char* vc = std::getenv("MPSP_CP");       // 0: register-prefetch kernel, 2: two stages
     if (!(vc && vc[0] == '0')) {
       constexpr int NC = L / 4;
-      const size_t smem = (size_t)4 * NC * CP_THREADS * 16;   // 2 stages x (a, x): 16L KB
-      static std::atomic<uint64_t> attr{0};
-      if (int e = ensure_smem_attr((const void*)spmv_sell_cp<L>, smem, attr)) return e;
-      spmv_sell_cp<L><<<(unsigned)blocks, CP_THREADS, smem, st>>>(P, x, y);
+      if (vc && vc[0] == '2') {                    // two stages (round 1 kernel)
+        const size_t smem = (size_t)4 * NC * CP_THREADS * 16;   // 2 stages x (a, x): 16L KB
+        static std::atomic<uint64_t> attr{0};
+        if (int e = ensure_smem_attr((const void*)spmv_sell_cp<L>, smem, attr)) return e;
+        spmv_sell_cp<L><<<(unsigned)blocks, CP_THREADS, smem, st>>>(P, x, y);
+        g_launches.fetch_add(1);
+        return (int)cudaGetLastError();
+      }
+      const size_t smem = (size_t)3 * NC * CP_THREADS * 16;     // a, x, parked s: 12L KB
+      static std::atomic<uint64_t> attr1{0};
+      if (int e = ensure_smem_attr((const void*)spmv_sell_cp1<L, 4>, smem, attr1)) return e;
+      spmv_sell_cp1<L, 4><<<(unsigned)blocks, CP_THREADS, smem, st>>>(P, x, y);
+      g_launches.fetch_add(1);
+      return (int)cudaGetLastError();
+    }
+  }
+  if constexpr (L == 8 || L == 16) {
+    // MPSP_CPS=<minb> (tuning knob, 4..8): the one-stage cp.async kernel
+    const char* vs = std::getenv("MPSP_CPS");
+    if (vs && vs[0] >= '4' && vs[0] <= '8') {
+      constexpr int NC = L / 4;
+      const size_t smem = (size_t)3 * NC * CP_THREADS * 16;
+      static std::atomic<uint64_t> a4{0}, a5{0}, a6{0}, a8{0};
+      int e = 0;
+      const unsigned nb = (unsigned)blocks;
+      switch (vs[0]) {
+        case '4': e = ensure_smem_attr((const void*)spmv_sell_cp1<L, 4>, smem, a4);
+                  if (!e) spmv_sell_cp1<L, 4><<<nb, CP_THREADS, smem, st>>>(P, x, y); break;
+        case '5': e = ensure_smem_attr((const void*)spmv_sell_cp1<L, 5>, smem, a5);
+                  if (!e) spmv_sell_cp1<L, 5><<<nb, CP_THREADS, smem, st>>>(P, x, y); break;
+        case '6': e = ensure_smem_attr((const void*)spmv_sell_cp1<L, 6>, smem, a6);
+                  if (!e) spmv_sell_cp1<L, 6><<<nb, CP_THREADS, smem, st>>>(P, x, y); break;
+        default:  e = ensure_smem_attr((const void*)spmv_sell_cp1<L, 8>, smem, a8);
+                  if (!e) spmv_sell_cp1<L, 8><<<nb, CP_THREADS, smem, st>>>(P, x, y); break;
+      }
+      if (e) return e;
       g_launches.fetch_add(1);
       return (int)cudaGetLastError();
     }
