@@ -56,20 +56,39 @@ struct WEntry {
   uint32_t sx;
 };
 
-// Step U*lane + u of chunk c (entry position e0 + c*32U + 32u + lane, the
+// Step U*lane + u of chunk c: entry position e0 + c*32U + 32u + lane (the
 // chunk-permuted warp-row layout of layout.h: a warp's 32 loads of one u are
-// consecutive entries).  Invalid steps (past the row end) load zero limbs.
+// consecutive entries), i.e. offset `off` = c*32U + 32u from the lane's base
+// pointers (32-bit offsets, no 64-bit index arithmetic per step).  Invalid
+// steps (past the row end) load zero limbs.
 template <int L>
-__device__ __forceinline__ void wload(const PartView& P, const XView& x, int64_t pos, bool valid,
-                                      int col, int lane, WEntry<L>& E) {
+struct WRowBase {
+  using CT = typename Chunk<L>::T;
+  static constexpr int NC = L / Chunk<L>::CW;
+  const int32_t* expw;   // + e0 + lane
+  const int32_t* col;    // + e0 + lane
+  const CT* a;           // chunk (e0/32, c = 0, lane)
+  __device__ __forceinline__ void init(const PartView& P, int64_t e0, int lane) {
+    expw = P.expw + e0 + lane;
+    col = P.col + e0 + lane;
+    a = reinterpret_cast<const CT*>(P.limbs) + (e0 >> 5) * NC * 32 + lane;
+  }
+};
+
+template <int L>
+__device__ __forceinline__ void wload(const WRowBase<L>& B, const XView& x, int off, bool valid,
+                                      int col, WEntry<L>& E) {
   if (!valid) {
 #pragma unroll
     for (int i = 0; i < L; ++i) { E.a[i] = 0u; E.x[i] = 0u; }
     E.w = 0; E.ex = 0; E.sx = 0u;
     return;
   }
-  E.w = __ldg(P.expw + pos);
-  load_a<L>(P.limbs, pos >> 5, lane, E.a);
+  constexpr int NC = WRowBase<L>::NC, CW = Chunk<L>::CW;
+  E.w = __ldg(B.expw + off);
+  const typename Chunk<L>::T* ap = B.a + (off >> 5) * (NC * 32);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) unpack_chunk(__ldg(ap + c * 32), &E.a[c * CW]);
   load_x<L>(x.limbs, col, E.x);
   E.ex = __ldg(x.exps + col);
   E.sx = __ldg(x.signs + col);
@@ -99,11 +118,13 @@ __global__ void __launch_bounds__(128, (L <= 8 ? MPSP_WROW_MINB : 1)) spmv_wrow(
   const int nch = (len + CS - 1) / CS;
   WChain<L> ch;
   ch.init();
+  WRowBase<L> B;
+  B.init(P, e0, lane);
   auto valid = [&](int c, int u) { return c * CS + U * lane + u < len; };
   auto colof = [&](int c, int u) -> int {
     if (!valid(c, u)) return 0;
     if constexpr (DENSE) return c * CS + U * lane + u;
-    return __ldg(P.col + e0 + c * CS + 32 * u + lane);
+    return __ldg(B.col + c * CS + 32 * u);
   };
   MP<L> t[U];
   if constexpr (L <= 16) {
@@ -112,7 +133,7 @@ __global__ void __launch_bounds__(128, (L <= 8 ? MPSP_WROW_MINB : 1)) spmv_wrow(
     int cn[U];
     if (nch > 0) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) wload<L>(P, x, e0 + 32 * u + lane, valid(0, u), colof(0, u), lane, nxt[u]);
+      for (int u = 0; u < U; ++u) wload<L>(B, x, 32 * u, valid(0, u), colof(0, u), nxt[u]);
 #pragma unroll
       for (int u = 0; u < U; ++u) cn[u] = colof(1, u);
     }
@@ -121,7 +142,7 @@ __global__ void __launch_bounds__(128, (L <= 8 ? MPSP_WROW_MINB : 1)) spmv_wrow(
       for (int u = 0; u < U; ++u) {
         const WEntry<L> cur = nxt[u];
         if (c + 1 < nch) {
-          wload<L>(P, x, e0 + (c + 1) * CS + 32 * u + lane, valid(c + 1, u), cn[u], lane, nxt[u]);
+          wload<L>(B, x, (c + 1) * CS + 32 * u, valid(c + 1, u), cn[u], nxt[u]);
           cn[u] = colof(c + 2, u);
         }
         const int32_t ea = (int32_t)((uint32_t)cur.w << 1) >> 1;
@@ -141,7 +162,7 @@ __global__ void __launch_bounds__(128, (L <= 8 ? MPSP_WROW_MINB : 1)) spmv_wrow(
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         WEntry<L> cur;
-        wload<L>(P, x, e0 + c * CS + 32 * u + lane, valid(c, u), cn[u], lane, cur);
+        wload<L>(B, x, c * CS + 32 * u, valid(c, u), cn[u], cur);
         cn[u] = colof(c + 1, u);
         const int32_t ea = (int32_t)((uint32_t)cur.w << 1) >> 1;
         mp_mul<L>(cur.a, ea, (uint32_t)cur.w >> 31, cur.x, cur.ex, cur.sx, t[u]);

@@ -26,6 +26,13 @@ __device__ __forceinline__ int32_t hi_of_q(const uint32_t (&Q)[L + 2]) {
   return (int32_t)__funnelshift_r(Q[L - 1], Q[L], 32 - HB);
 }
 
+// a - b saturated to the int32 range (exponent differences: |a|, |b| < 2^31)
+__device__ __forceinline__ int32_t sub_sat(int32_t a, int32_t b) {
+  int32_t d;
+  asm("sub.sat.s32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
 template <int N>
 __device__ __forceinline__ void warp_sum_limbs(uint32_t (&S)[N]) {
 #pragma unroll
@@ -134,10 +141,10 @@ struct WChain {
         continue;
       }
       const bool act = (lane >= start) && !tz;
-      const int64_t d64 = (int64_t)E - (int64_t)t.e;
-      const bool badd = act && d64 < 1;              // |t| >= 2^(E-1): leaves the binade
+      const int32_t d32 = sub_sat(E, t.e);            // E - t.e, saturated to int32
+      const bool badd = act && d32 < 1;              // |t| >= 2^(E-1): leaves the binade
       const bool use = act && !badd;
-      const uint32_t dd = use ? (uint32_t)min(d64, (int64_t)(32 * L + 32)) : 0u;
+      const uint32_t dd = use ? (uint32_t)min(d32, 32 * L + 32) : 0u;
       // Y = |t| / u  as integer limbs Y[1..L] and guard limb Y[0]
       uint32_t Y[L + 1];
       Y[0] = 0u;
@@ -164,16 +171,19 @@ struct WChain {
           inc = pS ^ lsbY;                            // make S_k even
         }
       }
-      // Q = +-(Y + inc) in N-limb two's complement, one carry chain:
-      // -(Y + inc) = ~Y + (1 - inc)
+      // Q = +-(Y + inc) in N-limb two's complement = P + cin with P = Y ^ nm
+      // (one's complement for the minus sign) and cin = inc or 1 - inc: the
+      // carry-in is added by the commit's own carry chain.  The high part h
+      // is taken from P, so Q/H lies in [h, h + 2): the bounds below count
+      // two units of error per step.
       const uint32_t neg = (use && t.s != sg) ? 1u : 0u;
-      const uint32_t nm = 0u - neg;
+      const uint32_t nm = 0u - neg, um = use ? ~0u : 0u;
+      const uint32_t cin = use ? (neg ? 1u - inc : inc) : 0u;
       uint32_t Q[N];
 #pragma unroll
-      for (int i = 0; i < L; ++i) Q[i] = (use ? Y[i + 1] : 0u) ^ nm;
+      for (int i = 0; i < L; ++i) Q[i] = (Y[i + 1] & um) ^ nm;
       Q[L] = nm;
       Q[L + 1] = nm;
-      inc_n<N>(Q, use ? (neg ? 1u - inc : inc) : 0u);
       const int32_t h = hi_of_q<L>(Q);
       int32_t Pi = h;                                 // inclusive scan of h
 #pragma unroll
@@ -182,26 +192,26 @@ struct WChain {
         if (lane >= o) Pi += v;
       }
       const int32_t LB = Shi + (Pi - h);              // S_{k-1}/H >= LB
-      const int32_t ek = err + lane;                  // S_{k-1}/H < LB + ek
-      const bool ok = !act || (!badd && LB + h - 1 >= LO && LB + ek + h + 1 <= HI);
+      const int32_t ek = err + 2 * lane;              // S_{k-1}/H < LB + ek
+      const bool ok = !act || (!badd && LB + h - 1 >= LO && LB + ek + h + 2 <= HI);
       const unsigned failM = __ballot_sync(FULL, !ok);
       if (failM == 0u) {
-        add_n<N>(R, R, Q);
+        add_n_cin<N>(R, R, Q, cin);
         Shi += __shfl_sync(FULL, Pi, 31);
-        err = min(err + 32, 1 << 28);                 // saturates: checks then fail
+        err = min(err + 64, 1 << 28);                 // saturates: checks then fail
         break;
       }
       // ---- the first failing step f
       const int f = __ffs(failM) - 1;
-      if (lane < f) add_n<N>(R, R, Q);               // steps before f are valid
-      step_f(t, f, __shfl_sync(FULL, LB, f), __shfl_sync(FULL, h, f), err + f, lane);
+      if (lane < f) add_n_cin<N>(R, R, Q, cin);      // steps before f are valid
+      step_f(t, f, __shfl_sync(FULL, LB, f), __shfl_sync(FULL, h, f), err + 2 * f, lane);
       start = f + 1;
     }
   }
 
   // The first failing step f of a block: lane f holds its product t; LBf, hf,
-  // ekf are its high-part bounds (S_{f-1}/H in [LBf, LBf + ekf), h_f =
-  // floor(Q_f / H)).  One-binade transitions (tests/test_kernel_algorithms.py
+  // ekf are its high-part bounds (S_{f-1}/H in [LBf, LBf + ekf), Q_f/H in
+  // [hf, hf + 2)).  One-binade transitions (tests/test_kernel_algorithms.py
   // models them): if step f's exact sum V = S + tau provably crosses 2^p
   // (equal signs) or provably lands in [2^(p-2), 2^(p-1)) (opposite signs),
   // it is rounded directly on the new grid 2u / u/2 from the low bits of
@@ -229,7 +239,7 @@ struct WChain {
       const uint32_t fy = Y[0];                     // tau's 32 fraction bits
       const bool fnz = (fy != 0u) || (stk != 0u);   // fraction != 0
       const bool up_f = use && t.s == sg && LBf + hf - 1 >= HI;
-      const bool dn_f = use && t.s != sg && LBf + ekf + hf + 2 <= LO && LBf + hf - 1 >= LO / 2;
+      const bool dn_f = use && t.s != sg && LBf + ekf + hf + 3 <= LO && LBf + hf - 1 >= LO / 2;
       // dominant product (|t| >= 2^(E-1), t.e - E = dd in [0, 27]): the binade
       // E + k of V = S u + t certified from the high-part bounds and t's top
       // 32 bits (units 2^(E-HB)); t/u = M_t 2^dd is an integer
@@ -317,7 +327,7 @@ struct WChain {
         }
         E += 1;
         Shi = (LBf + hf - 1) >> 1;
-        err = ((ekf + 3) >> 1) + 2;
+        err = ((ekf + 4) >> 1) + 2;
         return;
       }
       if (mode == 2) {                              // V in [2^(p-2), 2^(p-1)): grid u/2
@@ -347,7 +357,7 @@ struct WChain {
         }
         E -= 1;
         Shi = 2 * (LBf + hf - 1) - 2;
-        err = 2 * (ekf + 2) + 4;
+        err = 2 * (ekf + 3) + 4;
         return;
       }
     }
