@@ -64,6 +64,23 @@ struct DevPart {
   int32_t* expw = nullptr;
   uint32_t* limbs = nullptr;
   size_t bytes = 0;
+  // row chunks (host pipeline of mpsp_spmv_host): chunk c = local rows
+  // [crow[c], crow[c+1]), its SELL slices [cslice[c], cslice[c+1]); its rows
+  // read x only below chi[c].  One chunk unless build_part chunked the part.
+  std::vector<int64_t> crow, cslice, chi;
+
+  // the part restricted to chunk c's SELL slices (no warp rows)
+  PartView chunk_view(int c) const {
+    PartView v = view();
+    const int64_t s0 = cslice[(size_t)c], s1 = cslice[(size_t)c + 1];
+    v.slice_ptr = slice_ptr + s0;
+    v.slot_row = slot_row + 32 * s0;
+    v.slot_len = slot_len + 32 * s0;
+    v.nslices = s1 - s0;
+    v.nslots = 32 * (s1 - s0);
+    v.nwrow = 0;
+    return v;
+  }
 
   PartView view() const {
     PartView v;
@@ -97,8 +114,10 @@ struct mpsp_csr {
   // fork/join for running the long-row and short-row kernels concurrently
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  // host-buffer API workspace (lazily allocated)
-  cudaStream_t stream = nullptr;
+  // host-buffer API workspace (lazily allocated): compute stream, copy
+  // streams and per-chunk events of the H2D / kernels / D2H pipeline
+  cudaStream_t stream = nullptr, s_h2d = nullptr, s_d2h = nullptr;
+  std::vector<cudaEvent_t> ev_x, ev_y;
   void* ws = nullptr;
   size_t ws_bytes = 0;
 };
@@ -140,6 +159,34 @@ int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32
   const int64_t T = (wide || dense) ? -1 : (tv || nrows >= 32768 ? long_row_threshold() : 32);
   int64_t nw = 0;
   while (nw < nrows && lrp[order[(size_t)nw] + 1] - lrp[order[(size_t)nw]] > T) ++nw;
+  // Row chunks: a part of short rows only (no warp rows) with many rows is
+  // length-sorted within C contiguous row chunks instead of globally, so the
+  // host-buffer entry point can pipeline H2D of x, the chunk kernels and D2H
+  // of y (mpsp_spmv_host); short rows make the sort scope irrelevant to the
+  // device path.  Env MPSP_CHUNKS overrides C (1: no chunks).
+  int64_t C = 1;
+  if (nw == 0 && !wide && !dense && nrows >= 2 * 65536) C = std::min<int64_t>(8, nrows / 65536);
+  if (const char* vc = std::getenv("MPSP_CHUNKS")) C = std::max<int64_t>(1, std::min<int64_t>(64, std::atoll(vc)));
+  if (nw > 0 || wide || dense || nrows == 0) C = 1;
+  P.crow.assign((size_t)C + 1, 0);
+  P.chi.assign((size_t)C, 0);
+  for (int64_t c = 0; c <= C; ++c) P.crow[(size_t)c] = nrows * c / C;
+  if (C > 1) {
+    for (int64_t c = 0; c < C; ++c) {               // stable counting sort per chunk
+      const int64_t r0 = P.crow[(size_t)c], r1 = P.crow[(size_t)c + 1];
+      std::fill(cnt.begin(), cnt.end(), 0);
+      for (int64_t r = r0; r < r1; ++r) cnt[(size_t)(maxlen - (lrp[r + 1] - lrp[r]))]++;
+      int64_t a2 = r0;
+      for (auto& cc : cnt) { int64_t t = cc; cc = a2; a2 += t; }
+      for (int64_t r = r0; r < r1; ++r) order[(size_t)cnt[(size_t)(maxlen - (lrp[r + 1] - lrp[r]))]++] = (int32_t)r;
+    }
+  }
+  for (int64_t c = 0; c < C; ++c) {                 // x window end of each chunk
+    int64_t hi = 0;
+    for (int64_t r = P.crow[(size_t)c]; r < P.crow[(size_t)c + 1]; ++r)
+      if (lrp[r + 1] > lrp[r]) hi = std::max<int64_t>(hi, (int64_t)lcol[lrp[r + 1] - 1 - lrp[0]] + 1);
+    P.chi[(size_t)c] = hi;
+  }
   P.nwrow = nw;
   std::vector<int64_t> wptr((size_t)nw);
   std::vector<int32_t> wrow((size_t)nw), wlen((size_t)nw);
@@ -152,25 +199,36 @@ int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32
     const int64_t cs = wide ? 1 : 32 * wrow_spl(L);
     ew += (wlen[(size_t)i] + cs - 1) / cs * cs;
   }
-  // SELL slices of the remaining rows
-  const int64_t nshort = nrows - nw;
-  const int64_t nslices = (nshort + 31) / 32;
+  // SELL slices of the remaining rows (chunk by chunk: a chunk's last slice
+  // may be partial)
+  P.cslice.assign((size_t)C + 1, 0);
+  int64_t nslices = 0;
+  for (int64_t c = 0; c < C; ++c) {
+    const int64_t m = (c == 0 ? P.crow[1] - nw : P.crow[(size_t)c + 1] - P.crow[(size_t)c]);
+    P.cslice[(size_t)c] = nslices;
+    nslices += (m + 31) / 32;
+  }
+  P.cslice[(size_t)C] = nslices;
   P.nslices = nslices;
   std::vector<int64_t> sp((size_t)nslices + 1, 0);
   std::vector<int32_t> srow((size_t)nslices * 32, -1), slen((size_t)nslices * 32, 0);
   sp[0] = ew;
-  for (int64_t s = 0; s < nslices; ++s) {
-    int64_t w = 0;
-    for (int l = 0; l < 32; ++l) {
-      int64_t slot = s * 32 + l;
-      if (slot < nshort) {
-        int32_t r = order[(size_t)(nw + slot)];
-        srow[(size_t)slot] = r;
-        slen[(size_t)slot] = (int32_t)(lrp[r + 1] - lrp[r]);
-        w = std::max<int64_t>(w, slen[(size_t)slot]);
+  for (int64_t c = 0; c < C; ++c) {
+    const int64_t o0 = (c == 0 ? nw : P.crow[(size_t)c]), o1 = P.crow[(size_t)c + 1];
+    for (int64_t s = P.cslice[(size_t)c]; s < P.cslice[(size_t)c + 1]; ++s) {
+      int64_t w = 0;
+      for (int l = 0; l < 32; ++l) {
+        const int64_t slot = s * 32 + l;
+        const int64_t oi = o0 + (s - P.cslice[(size_t)c]) * 32 + l;
+        if (oi < o1) {
+          int32_t r = order[(size_t)oi];
+          srow[(size_t)slot] = r;
+          slen[(size_t)slot] = (int32_t)(lrp[r + 1] - lrp[r]);
+          w = std::max<int64_t>(w, slen[(size_t)slot]);
+        }
       }
+      sp[(size_t)s + 1] = sp[(size_t)s] + 32 * w;
     }
-    sp[(size_t)s + 1] = sp[(size_t)s] + 32 * w;
   }
   const int64_t nent = sp[(size_t)nslices];
   P.nentries = nent;
@@ -545,6 +603,10 @@ void mpsp_destroy(mpsp_csr* A) {
   A->T.release();
   if (A->ws) cudaFree(A->ws);
   if (A->stream) cudaStreamDestroy(A->stream);
+  if (A->s_h2d) cudaStreamDestroy(A->s_h2d);
+  if (A->s_d2h) cudaStreamDestroy(A->s_d2h);
+  for (cudaEvent_t e : A->ev_x) cudaEventDestroy(e);
+  for (cudaEvent_t e : A->ev_y) cudaEventDestroy(e);
   if (A->aux) cudaStreamDestroy(A->aux);
   if (A->ev_fork) cudaEventDestroy(A->ev_fork);
   if (A->ev_join) cudaEventDestroy(A->ev_join);
@@ -604,18 +666,69 @@ static int spmv_host(mpsp_csr* A, bool transpose, const uint32_t* xl, const int3
   size_t off = 0;
   for (int i = 0; i < 3; ++i) { dx[i] = base + off; off += al(xb[i]); }
   for (int i = 0; i < 3; ++i) { dy[i] = base + off; off += al(yb[i]); }
-  for (int i = 0; i < 3; ++i)
-    if (xb[i] && (e = cudaMemcpyAsync(dx[i], xp[i], xb[i], cudaMemcpyHostToDevice, A->stream)) != cudaSuccess)
+  const DevPart& P = transpose ? A->T : A->A;
+  const int64_t C = (int64_t)P.crow.size() - 1;
+  if (C <= 1 || L > 32 || A->dense) {
+    for (int i = 0; i < 3; ++i)
+      if (xb[i] && (e = cudaMemcpyAsync(dx[i], xp[i], xb[i], cudaMemcpyHostToDevice, A->stream)) != cudaSuccess)
+        return cuda_fail(e);
+    int rc = do_spmv(A, transpose, (const uint32_t*)dx[0], (const int32_t*)dx[1], (const uint8_t*)dx[2],
+                     (uint32_t*)dy[0], (int32_t*)dy[1], (uint8_t*)dy[2], A->stream, false);
+    if (rc) return rc;
+    void* hy[3] = {yl, ye, ys};
+    for (int i = 0; i < 3; ++i)
+      if (yb[i] && (e = cudaMemcpyAsync(hy[i], dy[i], yb[i], cudaMemcpyDeviceToHost, A->stream)) != cudaSuccess)
+        return cuda_fail(e);
+    e = cudaStreamSynchronize(A->stream);
+    return e == cudaSuccess ? MPSP_OK : cuda_fail(e);
+  }
+  // Row-chunk pipeline: chunk c's kernels start once x is
+  // on the device up to the chunk's window end chi[c] (H2D in increasing
+  // index order on s_h2d), and its y rows go back on s_d2h while the next
+  // chunks compute - H2D, kernels and D2H overlap (full duplex on the link).
+  if (!A->s_h2d) {
+    if ((e = cudaStreamCreateWithFlags(&A->s_h2d, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&A->s_d2h, cudaStreamNonBlocking)) != cudaSuccess)
       return cuda_fail(e);
-  int rc = do_spmv(A, transpose, (const uint32_t*)dx[0], (const int32_t*)dx[1], (const uint8_t*)dx[2],
-                   (uint32_t*)dy[0], (int32_t*)dy[1], (uint8_t*)dy[2], A->stream, false);
-  if (rc) return rc;
-  void* hy[3] = {yl, ye, ys};
-  for (int i = 0; i < 3; ++i)
-    if (yb[i] && (e = cudaMemcpyAsync(hy[i], dy[i], yb[i], cudaMemcpyDeviceToHost, A->stream)) != cudaSuccess)
+  }
+  while ((int64_t)A->ev_x.size() < C) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if ((e = cudaEventCreateWithFlags(&a, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaEventCreateWithFlags(&b, cudaEventDisableTiming)) != cudaSuccess) {
+      cudaEventDestroy(a);
       return cuda_fail(e);
-  e = cudaStreamSynchronize(A->stream);
-  if (e != cudaSuccess) return cuda_fail(e);
+    }
+    A->ev_x.push_back(a);
+    A->ev_y.push_back(b);
+  }
+  XView xv{(const uint32_t*)dx[0], (const int32_t*)dx[1], (const uint8_t*)dx[2]};
+  YView yv{(uint32_t*)dy[0], (int32_t*)dy[1], (uint8_t*)dy[2]};
+  int64_t copied = 0, xneed = 0;
+  const size_t esz[3] = {(size_t)L * 4, 4, 1};
+  for (int64_t c = 0; c < C; ++c) {
+    xneed = std::min<int64_t>(n, std::max<int64_t>(xneed, P.chi[(size_t)c]));
+    if (xneed > copied) {
+      for (int i = 0; i < 3; ++i)
+        if ((e = cudaMemcpyAsync((char*)dx[i] + copied * esz[i], (const char*)xp[i] + copied * esz[i],
+                                 (size_t)(xneed - copied) * esz[i], cudaMemcpyHostToDevice, A->s_h2d)) != cudaSuccess)
+          return cuda_fail(e);
+      copied = xneed;
+    }
+    if ((e = cudaEventRecord(A->ev_x[(size_t)c], A->s_h2d)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaStreamWaitEvent(A->stream, A->ev_x[(size_t)c], 0)) != cudaSuccess) return cuda_fail(e);
+    const int err = launch_spmv(L, P.chunk_view((int)c), xv, yv, A->stream);
+    if (err) return cuda_fail((cudaError_t)err);
+    if ((e = cudaEventRecord(A->ev_y[(size_t)c], A->stream)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaStreamWaitEvent(A->s_d2h, A->ev_y[(size_t)c], 0)) != cudaSuccess) return cuda_fail(e);
+    const int64_t r0 = P.crow[(size_t)c], r1 = P.crow[(size_t)c + 1];
+    void* hy[3] = {yl, ye, ys};
+    for (int i = 0; i < 3; ++i)
+      if (r1 > r0 && (e = cudaMemcpyAsync((char*)hy[i] + r0 * esz[i], (const char*)dy[i] + r0 * esz[i],
+                                          (size_t)(r1 - r0) * esz[i], cudaMemcpyDeviceToHost, A->s_d2h)) != cudaSuccess)
+        return cuda_fail(e);
+  }
+  if ((e = cudaStreamSynchronize(A->s_d2h)) != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaStreamSynchronize(A->stream)) != cudaSuccess) return cuda_fail(e);
   return MPSP_OK;
 }
 

@@ -334,3 +334,34 @@ def test_interior_boundary_split_emulated(cfg, n, op):
         assert_same(cat, want, f"{cfg} G={G} {op} interior/boundary")
         if cfg in ("C5", "C2"):
             assert n_inner > n // 2            # banded / stencil blocks are mostly interior
+
+
+@pytest.mark.parametrize("chunks", ["1", "3", "7"])
+@pytest.mark.parametrize("cfg,n,op", [("C5", 4900, "ax"), ("C3", 3000, "ax"), ("C2", 5000, "atx"),
+                                      ("C1", 700, "ax"), ("C4", 4000, "atx")])
+def test_row_chunks_device_and_host_pipeline(cfg, n, op, chunks, monkeypatch):
+    """Row-chunked layout (rows length-sorted within C contiguous chunks,
+    env MPSP_CHUNKS forcing C on small matrices) and the host-buffer
+    pipeline of mpsp_spmv_host (per chunk: H2D of x up to the chunk's window
+    end, the chunk's kernels, D2H of its y rows, on three streams) - both
+    bit-exact against the oracle, from pinned and pageable host buffers."""
+    import torch
+    monkeypatch.setenv("MPSP_CHUNKS", chunks)
+    d = gen.make(cfg, n=n, seed=31)
+    want = oracle_full(d, op)
+    A = _csr(d, transpose=(op == "atx"))
+    x = _x(d)
+    assert_same((A.spmv if op == "ax" else A.spmv_t)(x).to_host(), want, f"device chunks={chunks}")
+    f = A.spmv_host if op == "ax" else A.spmv_t_host
+    assert_same(f(d["x_limbs"], d["x_exps"], d["x_signs"]), want, f"host pageable chunks={chunks}")
+    L = d["p"] // 32
+    hx = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+          for a in (d["x_limbs"].view(np.int32), d["x_exps"], d["x_signs"])]
+    hx[0] = hx[0].view(np.uint32)
+    hy = (torch.empty((d["n"], L), dtype=torch.int32).pin_memory().numpy().view(np.uint32),
+          torch.empty(d["n"], dtype=torch.int32).pin_memory().numpy(),
+          torch.empty(d["n"], dtype=torch.uint8).pin_memory().numpy())
+    for _ in range(2):
+        f(*hx, out=hy)
+        assert_same(hy, want, f"host pinned chunks={chunks}")
+    A.close()
