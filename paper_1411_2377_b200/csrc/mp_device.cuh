@@ -241,6 +241,14 @@ __device__ __forceinline__ uint32_t comba_lower(const uint32_t (&a)[L], const ui
 // are formed too and their carry added in: the exact product.
 // Executed limb-MACs on the fast path: L^2 - (L-3)(L-2)/2 (L=32: 618 of 1024).
 // --------------------------------------------------------------------------
+// The rounding half of mp_mul: T = comba_upper<L, L-3>(a, x) (limbs L-3 ..
+// 2L-1 of the product's upper columns) -> t.  Split out so a caller can
+// form T for the next entry in the same basic block as other work.
+template <int L>
+__device__ __forceinline__ void mp_mul_finish(const uint32_t (&a)[L], int32_t ea, uint32_t sa,
+                                              const uint32_t (&x)[L], int32_t ex, uint32_t sx,
+                                              uint32_t (&T)[L + 3], MP<L>& t);
+
 template <int L>
 __device__ __forceinline__ void mp_mul(const uint32_t (&a)[L], int32_t ea, uint32_t sa,
                                        const uint32_t (&x)[L], int32_t ex, uint32_t sx,
@@ -248,9 +256,18 @@ __device__ __forceinline__ void mp_mul(const uint32_t (&a)[L], int32_t ea, uint3
   if constexpr (L < 4) {
     mp_mul_full<L>(a, ea, sa, x, ex, sx, t);
   } else {
-    constexpr int K0 = L - 3;
     uint32_t T[L + 3];                               // limbs L-3 .. 2L-1
-    comba_upper<L, K0>(a, x, T);
+    comba_upper<L, L - 3>(a, x, T);
+    mp_mul_finish<L>(a, ea, sa, x, ex, sx, T, t);
+  }
+}
+
+template <int L>
+__device__ __forceinline__ void mp_mul_finish(const uint32_t (&a)[L], int32_t ea, uint32_t sa,
+                                              const uint32_t (&x)[L], int32_t ex, uint32_t sx,
+                                              uint32_t (&T)[L + 3], MP<L>& t) {
+  {
+    constexpr int K0 = L - 3;
     uint32_t sh = (~T[L + 2]) >> 31;                 // top product bit clear -> 1
     const uint32_t wmask = (1u << (31u - sh)) - 1u;  // T[2] bits below the round bit
     const uint32_t w1 = T[1] >> 5, w2 = T[2] & wmask;

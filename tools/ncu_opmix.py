@@ -31,4 +31,7 @@ for r in rows[2:]:
 tot = sum(c.values())
 print(f"total {tot} ({tot / per:.1f} per unit)")
 for op, n in c.most_common(40):
-    print(f"{op:28s} {n:12d} {n / per:8.1f}")
+    try:
+        print(f"{op:28s} {n:12d} {n / per:8.1f}")
+    except BrokenPipeError:
+        break
