@@ -54,8 +54,7 @@ __global__ void __launch_bounds__(128, MINB) spmv_sell(PartView P, XView x, YVie
   auto step = [&](const uint32_t (&a)[L], const uint32_t (&xv)[L], int32_t w, int32_t ex,
                   uint32_t sx, bool first) {
     MP<L> t;
-    const int32_t ea = (int32_t)((uint32_t)w << 1) >> 1;
-    mp_mul<L>(a, ea, (uint32_t)w >> 31, xv, ex, sx, t);
+    mul_entry<L>(a, w, xv, ex, sx, t);
     if (first) {                     // RN(+0 + t) = t: the first add is a copy
       s = t;                         // (warp-uniform: all lanes are at step j)
     } else {
@@ -182,8 +181,7 @@ __global__ void __launch_bounds__(CP_THREADS, CpMinB<L>::v) spmv_sell_cp(PartVie
       for (int c = 0; c < NC; ++c)
         *sa(u, c) = make_uint4(s.m[4 * c], s.m[4 * c + 1], s.m[4 * c + 2], s.m[4 * c + 3]);
       MP<L> t;
-      const int32_t ea = (int32_t)((uint32_t)wq[u] << 1) >> 1;
-      mp_mul<L>(a, ea, (uint32_t)wq[u] >> 31, xv, exq[u], sq[u], t);
+      mul_entry<L>(a, wq[u], xv, exq[u], sq[u], t);
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         const uint4 v = *sa(u, c);
@@ -269,8 +267,7 @@ __global__ void __launch_bounds__(CP_THREADS, MINB) spmv_sell_cp1(PartView P, XV
     for (int c = 0; c < NC; ++c)
       *ss(c) = make_uint4(s.m[4 * c], s.m[4 * c + 1], s.m[4 * c + 2], s.m[4 * c + 3]);
     MP<L> t;
-    const int32_t ea = (int32_t)((uint32_t)wq << 1) >> 1;
-    mp_mul<L>(a, ea, (uint32_t)wq >> 31, xv, exq, sq, t);
+    mul_entry<L>(a, wq, xv, exq, sq, t);
     if (j + 1 < len) {                           // the slots are consumed: refill
       issue(j + 1, cn);
       cn = cn2;

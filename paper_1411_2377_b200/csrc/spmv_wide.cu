@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(32 * WARPS) spmv_wide(PartView P, XView x, YVi
     const uint32_t sxv = nsx;
     if (j + 1 < len) fetch(j + 1);
     WMP<K> t;
-    const int32_t ea = (int32_t)((uint32_t)wv << 1) >> 1;
+    const int32_t ea = expw_exp(wv);
     wmul<K>(a, ea, (uint32_t)wv >> 31, xv, exv, sxv, sA, sX, cs, lane, t);
     wadd<K>(s, t, cs, lane);
     __syncwarp();

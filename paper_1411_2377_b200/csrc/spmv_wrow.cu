@@ -145,8 +145,7 @@ __global__ void __launch_bounds__(128, (L <= 8 ? MPSP_WROW_MINB : 1)) spmv_wrow(
           wload<L>(B, x, (c + 1) * CS + 32 * u, valid(c + 1, u), cn[u], nxt[u]);
           cn[u] = colof(c + 2, u);
         }
-        const int32_t ea = (int32_t)((uint32_t)cur.w << 1) >> 1;
-        mp_mul<L>(cur.a, ea, (uint32_t)cur.w >> 31, cur.x, cur.ex, cur.sx, t[u]);
+        mul_entry<L>(cur.a, cur.w, cur.x, cur.ex, cur.sx, t[u]);
       }
       if constexpr (U == 1)
         ch.consume(t[0], lane);          // ties resolved from the running parity
@@ -164,8 +163,7 @@ __global__ void __launch_bounds__(128, (L <= 8 ? MPSP_WROW_MINB : 1)) spmv_wrow(
         WEntry<L> cur;
         wload<L>(B, x, c * CS + 32 * u, valid(c, u), cn[u], cur);
         cn[u] = colof(c + 1, u);
-        const int32_t ea = (int32_t)((uint32_t)cur.w << 1) >> 1;
-        mp_mul<L>(cur.a, ea, (uint32_t)cur.w >> 31, cur.x, cur.ex, cur.sx, t[u]);
+        mul_entry<L>(cur.a, cur.w, cur.x, cur.ex, cur.sx, t[u]);
       }
       if constexpr (U == 1)
         ch.consume(t[0], lane);          // ties resolved from the running parity

@@ -186,3 +186,42 @@ def test_warp_threshold_split_c4(thr, monkeypatch):
     d = gen.make("C4", n=20_000, seed=10)
     for op in ("ax", "atx"):
         assert_same(gpu_run(d, op), oracle_full(d, op), f"C4 warp threshold {thr} {op}")
+
+
+@pytest.mark.parametrize("p", [512, 1024])
+def test_power_of_two_entries(p):
+    """Rows whose k-th stored entry is a power of two (M = 2^(p-1)) at the same
+    step in every row of a warp: the kernels' exact shortcut (the product is
+    x with the exponent moved, kernel_common.cuh mul_entry) runs for whole
+    warps - with zero x, both signs, exponents at +-2^29 and a mix of warps
+    where only some lanes qualify."""
+    rng = np.random.default_rng(p)
+    L = p // 32
+    n = 700
+    rowptr, cols, vals = [0], [], []
+    top = 1 << (p - 1)
+    for i in range(n):
+        k = int(rng.integers(1, 6))
+        cs = sorted(rng.choice(n, size=k, replace=False).tolist())
+        for j, c in enumerate(cs):
+            if j == 0 or (i % 3 == 0 and j == 2):
+                e = int(rng.choice([-(1 << 29), (1 << 29), 0, 3, -7]))
+                vals.append((int(rng.integers(0, 2)), top, e))        # power of two
+            else:
+                vals.append((int(rng.integers(0, 2)), top | int(rng.integers(0, 1 << 62)) << 3,
+                             int(rng.integers(-20, 20))))
+        cols += cs
+        rowptr.append(len(cols))
+    limbs, exps, signs = gen.pack_triples(vals, p)
+    xv = []
+    for j in range(n):
+        if j % 7 == 0:
+            xv.append((0, 0, 0))
+        else:
+            xv.append((int(rng.integers(0, 2)), top | (int(rng.integers(0, 1 << 62)) << (p - 64)),
+                       int(rng.choice([-(1 << 29), (1 << 29) - 1, 5, -5]))))
+    xl, xe, xs = gen.pack_triples(xv, p)
+    d = dict(p=p, n=n, rowptr=np.array(rowptr, np.int64), colidx=np.array(cols, np.int32),
+             limbs=limbs, exps=exps, signs=signs, x_limbs=xl, x_exps=xe, x_signs=xs)
+    for op in ("ax", "atx"):
+        assert_same(gpu_run(d, op), oracle_full(d, op), f"pow2 p={p} {op}")
