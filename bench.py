@@ -301,7 +301,19 @@ def time_steps(f, x, y, stream, steps, warmup, flush_buf):
     return [a.elapsed_time(b) for a, b in evs]
 
 
-def roofline(meta, nrows, nnz, kern_s, int_peak, hbm_peak, peak_src):
+def pow2_fraction(d, op):
+    """Fraction of A's stored entries whose mantissa is exactly 2^(p-1) (at
+    p = 1024 the kernels form no product for a warp of such entries, DESIGN.md
+    "Product"; an upper bound of the skipped share - the whole warp must
+    qualify).  0 below p = 1024."""
+    if d["p"] != 1024 or len(d["limbs"]) == 0:
+        return 0.0
+    lm = np.asarray(d["limbs"]).reshape(-1, d["p"] // 32)
+    f = (lm[:, -1] == np.uint32(0x80000000)) & ~np.any(lm[:, :-1], axis=1)
+    return float(f.mean())
+
+
+def roofline(meta, nrows, nnz, kern_s, int_peak, hbm_peak, peak_src, skip=0.0):
     """Roofline of one application: t_roof = max(bytes/HBM,
     nnz L^2 / P_int); frac = t_roof / t_kernel (= achieved / peak of the
     binding resource)."""
@@ -322,8 +334,10 @@ def roofline(meta, nrows, nnz, kern_s, int_peak, hbm_peak, peak_src):
     r["hbm_achieved_gbs"] = bytes_ / kern_s / 1e9
     r["macs_achieved_T"] = macs / kern_s / 1e12
     r["algorithmic_bytes"] = bytes_
-    ex = executed_macs_per_nnz(L)
+    ex = executed_macs_per_nnz(L) * (1.0 - skip)
     r["executed_macs_per_nnz"] = ex
+    if skip:
+        r["power_of_two_entries"] = skip
     r["frac_executed"] = (nnz * ex / kern_s) / int_peak     # the IMAD pipe's own load
     return r
 
@@ -372,7 +386,8 @@ def per_config_block(args, dev, stream, flush_buf, int_peak, hbm_peak, peak_src,
             ms = time_steps(f, x, y, stream, max(args.steps, 10), max(args.warmup, 3), fb)
             clocks = sampler.stop()
             kern_s = statistics.median(ms) * 1e-3
-            r = roofline(d["meta"], n, nnz, kern_s, int_peak, hbm_peak, peak_src)
+            r = roofline(d["meta"], n, nnz, kern_s, int_peak, hbm_peak, peak_src,
+                         pow2_fraction(d, op))
             e = {"kernel_ms_median": statistics.median(ms), "kernel_ms_min": min(ms),
                  "kernel_ms_mean": sum(ms) / len(ms), "steps": len(ms),
                  "value": nnz / kern_s, "unit": UNIT, "limb_macs_per_s": nnz * L * L / kern_s,
@@ -573,7 +588,8 @@ def main():
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     peak_src = "MEASURED_PEAKS.json hbm_gbs" if peaks else "B200_PROFILING.md fallback"
     int_peak = ib["limb_macs_per_s"]
-    roof = roofline(d["meta"], re - rb, nnz_local, kern_avg_s, int_peak, hbm_peak, peak_src)
+    roof = roofline(d["meta"], re - rb, nnz_local, kern_avg_s, int_peak, hbm_peak, peak_src,
+                    pow2_fraction(d, args.op))
     # DRAM bytes per launch of the dominant kernel from the committed ncu
     # --set full capture of this workload (tools/traffic_from_ncu.py)
     roof["traffic"] = None

@@ -77,17 +77,18 @@ __device__ __forceinline__ void load_x(const uint32_t* __restrict__ xl, int col,
 __device__ __forceinline__ int32_t expw_exp(int32_t w) { return (int32_t)((uint32_t)w << 1) >> 1; }
 __device__ __forceinline__ uint32_t expw_sign(int32_t w) { return (uint32_t)w >> 31; }
 
-// t = RN(a_k * x_col) for one stored entry.  At L >= 16 a power-of-two a
+// t = RN(a_k * x_col) for one stored entry.  At L = 32 a power-of-two a
 // (M_a = 2^(p-1): the product is exact, t is x with the exponent moved) skips
 // the multiplication when every active lane's entry is one (a warp-uniform
 // branch; C5's diagonal 4 sits at the same step of every interior row).  The
-// test reads the loaded limbs (an OR over L-1 limbs, ~L/3 instructions).
+// test reads the loaded limbs (an OR over L-1 limbs, ~L/3 instructions; at
+// L = 16 it measured 8% slower on C3, whose entries are never powers of two).
 template <int L>
 __device__ __forceinline__ void mul_entry(const uint32_t (&a)[L], int32_t w, const uint32_t (&x)[L],
                                           int32_t ex, uint32_t sx, MP<L>& t) {
   const int32_t ea = expw_exp(w);
   const uint32_t sa = expw_sign(w);
-  if constexpr (L >= 16) {
+  if constexpr (L >= 32) {
     uint32_t lo = 0u;
 #pragma unroll
     for (int i = 0; i < L - 1; ++i) lo |= a[i];
