@@ -85,6 +85,12 @@ def run(seed):
     A.close()
     if not same(got, want):
         return f"spmv {op} p={p} n={n}"
+    if R.random() < 0.3:                                # host-buffer entry point
+        A = CSR(p, rowptr, colidx, limbs, exps, signs, transpose=(op == "atx"))
+        got = (A.spmv_host if op == "ax" else A.spmv_t_host)(xl, xe, xs)
+        A.close()
+        if not same(got, want):
+            return f"spmv_host {op} p={p} n={n}"
     if R.random() < 0.3 and n <= 120:                   # dense handle of the same matrix
         L = p // 32
         dl = np.zeros((n * n, L), np.uint32)
