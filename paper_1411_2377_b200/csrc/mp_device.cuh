@@ -319,11 +319,15 @@ template <int N>
 __device__ __forceinline__ void shr_bits_sticky(uint32_t (&v)[N], uint32_t d, uint32_t& sticky) {
   const uint32_t q = d >> 5, r = d & 31u;
   // limb steps only up to the largest limb shift any active lane needs
-  // (warp-uniform branch: no divergence, no dynamic register indexing)
-  const uint32_t qmax = __reduce_max_sync(__activemask(), q);
+  // (warp-uniform branch: no divergence, no dynamic register indexing); the
+  // one- and two-limb steps of short operands (N <= 17), which nearly every
+  // warp needs there, run unconditionally (a branch per level made ptxas copy
+  // the whole array at each merge; measured C4 -2%, C5 needs neither)
+  constexpr int UNC = N <= 17 ? 4 : 1;
+  const uint32_t qmax = N > UNC ? __reduce_max_sync(__activemask(), q) : 0u;
 #pragma unroll
   for (int b = 1; b <= N; b <<= 1) {
-    if (qmax >= (uint32_t)b) {
+    if (b < UNC || qmax >= (uint32_t)b) {
       const bool on = (q & (uint32_t)b) != 0u;
       uint32_t drop = 0u;
 #pragma unroll
