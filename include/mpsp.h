@@ -207,6 +207,20 @@ int mpsp_vec_pack(int p_bits, int64_t count, const uint32_t *limbs, const int32_
 int mpsp_vec_unpack(int p_bits, int64_t count, const uint32_t *rec, uint32_t *limbs,
                     int32_t *exps, uint8_t *signs, void *cuda_stream);
 
+/*
+ * mpsp_debug_host_build - the host half of mpsp_csr_create without a GPU:
+ * the same validation (same error codes), transpose, row binning, row chunks
+ * and repack, then a checksum of the device arrays instead of the upload.
+ * For host-side tests (address / undefined-behaviour sanitizers, SURVEY.md
+ * 4 T6).  out[0..5] = part A: nnz, stored entries incl. padding, warp rows,
+ * SELL slices, row chunks, checksum; out[6..11] = the same for A^T (zeros
+ * without MPSP_WITH_TRANSPOSE).  Errors: those of mpsp_csr_create except
+ * MPSP_E_CUDA; MPSP_E_ARG for out == NULL.
+ */
+int mpsp_debug_host_build(int p_bits, int64_t n, const int64_t *rowptr, const int32_t *colidx,
+                          const uint32_t *limbs, const int32_t *exps, const uint8_t *signs,
+                          int64_t row_begin, int64_t row_end, uint32_t flags, int64_t out[12]);
+
 /* Number of kernels this library has launched in this process (monotone). */
 int64_t mpsp_launch_count(void);
 

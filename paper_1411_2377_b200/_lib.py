@@ -25,7 +25,7 @@ SYMBOLS = ("mpsp_csr_create", "mpsp_dense_create", "mpsp_spmv", "mpsp_spmv_t", "
            "mpsp_destroy", "mpsp_strerror", "mpsp_last_cuda_error", "mpsp_csr_info",
            "mpsp_launch_count", "mpsp_imad_bench", "mpsp_supported_precision",
            "mpsp_dot", "mpsp_axpy", "mpsp_bicg", "mpsp_gpbicg", "mpsp_debug_dot_stats",
-           "mpsp_vec_pack", "mpsp_vec_unpack")
+           "mpsp_vec_pack", "mpsp_vec_unpack", "mpsp_debug_host_build")
 BICG_STATUS = {0: "converged", 1: "breakdown", 2: "max_iter"}
 
 
@@ -93,6 +93,8 @@ def lib() -> ctypes.CDLL:
     L.mpsp_vec_pack.restype = I
     L.mpsp_vec_unpack.argtypes = [I, I64, P, P, P, P, P]
     L.mpsp_vec_unpack.restype = I
+    L.mpsp_debug_host_build.argtypes = [I, I64, P, P, P, P, P, I64, I64, U32, ctypes.POINTER(I64)]
+    L.mpsp_debug_host_build.restype = I
     _lib = L
     return L
 

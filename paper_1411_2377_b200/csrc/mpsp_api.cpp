@@ -137,7 +137,7 @@ bool supported_L(int L) {
 template <class Dummy = void>
 int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32_t* lcol,
                const int64_t* srck, int64_t k0, const uint32_t* limbs, const int32_t* exps,
-               const uint8_t* signs, bool dense = false) {
+               const uint8_t* signs, bool dense = false, uint64_t* host_check = nullptr) {
   P.nrows = nrows;
   P.nnz = lrp[nrows] - lrp[0];
   // --- a3: stable counting sort of rows by length, descending
@@ -285,6 +285,20 @@ int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32
       }
     }
   });
+  if (host_check) {
+    // host-only build (mpsp_debug_host_build): no device memory; a checksum
+    // of the device arrays instead of the upload
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](const void* d, size_t bytes) {
+      const unsigned char* c = (const unsigned char*)d;
+      for (size_t i = 0; i < bytes; ++i) h = (h ^ c[i]) * 1099511628211ull;
+    };
+    mix(sp.data(), sp.size() * 8); mix(srow.data(), srow.size() * 4); mix(slen.data(), slen.size() * 4);
+    mix(wptr.data(), wptr.size() * 8); mix(wrow.data(), wrow.size() * 4); mix(wlen.data(), wlen.size() * 4);
+    mix(hcol.data(), hcol.size() * 4); mix(hexp.data(), hexp.size() * 4); mix(hl.data(), hl.size() * 4);
+    *host_check = h;
+    return MPSP_OK;
+  }
   // --- upload
   auto up = [&](void** dst, const void* src, size_t bytes) -> int {
     if (bytes == 0) bytes = 16;  // keep pointers valid for empty parts
@@ -488,18 +502,16 @@ int mpsp_dense_create(mpsp_csr** out, int p_bits, int64_t n, const uint32_t* lim
                      flags, true);
 }
 
-static int create_impl(mpsp_csr** out, int p_bits, int64_t n, const int64_t* rowptr,
-                       const int32_t* colidx, const uint32_t* limbs, const int32_t* exps,
-                       const uint8_t* signs, int64_t row_begin, int64_t row_end, uint32_t flags,
-                       bool dense) {
-  if (!out) return MPSP_E_ARG;
-  *out = nullptr;
+// a1: argument, CSR-invariant and value-encoding checks of mpsp_csr_create
+// (include/mpsp.h lists the codes).
+static int validate_csr(int p_bits, int64_t n, const int64_t* rowptr, const int32_t* colidx,
+                        const uint32_t* limbs, const int32_t* exps, const uint8_t* signs,
+                        int64_t row_begin, int64_t row_end, uint32_t flags) {
   if (n < 0 || !rowptr || row_begin < 0 || row_end < row_begin || row_end > n) return MPSP_E_ARG;
   if (flags & ~MPSP_WITH_TRANSPOSE) return MPSP_E_ARG;
   if (!mpsp_supported_precision(p_bits)) return MPSP_E_PREC;
   if (n > INT32_MAX) return MPSP_E_CSR;
   const int L = p_bits / 32;
-  // ---- a1: CSR invariants
   if (rowptr[0] != 0) return MPSP_E_CSR;
   for (int64_t i = 0; i < n; ++i)
     if (rowptr[i + 1] < rowptr[i]) return MPSP_E_CSR;
@@ -514,38 +526,37 @@ static int create_impl(mpsp_csr** out, int p_bits, int64_t n, const int64_t* row
   for (int64_t i = 0; i < n; ++i)
     for (int64_t k = rowptr[i] + 1; k < rowptr[i + 1]; ++k)
       if (colidx[k] <= colidx[k - 1]) return MPSP_E_UNSORTED;
-  // ---- value encodings
-  {
-    std::atomic<int> bad{0};
-    parallel_for(nnz, [&](int64_t k0, int64_t k1) {
-      for (int64_t k = k0; k < k1; ++k) {
-        const uint32_t* m = limbs + (size_t)k * L;
-        bool nz = false;
-        for (int c = 0; c < L; ++c) nz |= m[c] != 0u;
-        if (!nz) continue;
-        if (!(m[L - 1] >> 31) || exps[k] > (1 << 29) || exps[k] < -(1 << 29)) bad.store(1);
-      }
-    });
-    if (bad.load()) return MPSP_E_VALUE;
-  }
-  int dev = 0;
-  cudaError_t ce = cudaGetDevice(&dev);
-  if (ce != cudaSuccess) return cuda_fail(ce);
-  mpsp_csr* H = new (std::nothrow) mpsp_csr();
-  if (!H) return MPSP_E_NOMEM;
-  H->dev = dev; H->p = p_bits; H->L = L; H->n = n; H->rb = row_begin; H->re = row_end;
-  H->flags = flags;
-  H->dense = dense;
+  std::atomic<int> bad{0};
+  parallel_for(nnz, [&](int64_t k0, int64_t k1) {
+    for (int64_t k = k0; k < k1; ++k) {
+      const uint32_t* m = limbs + (size_t)k * L;
+      bool nz = false;
+      for (int c = 0; c < L; ++c) nz |= m[c] != 0u;
+      if (!nz) continue;
+      if (!(m[L - 1] >> 31) || exps[k] > (1 << 29) || exps[k] < -(1 << 29)) bad.store(1);
+    }
+  });
+  return bad.load() ? MPSP_E_VALUE : MPSP_OK;
+}
+
+// a2 + a3: rows [row_begin, row_end) of A, and of A^T with MPSP_WITH_TRANSPOSE
+// (stable counting sort on column: ascending row index of A inside each
+// transposed row), binned and repacked.  check != nullptr: host only (no
+// device memory), check[0] / check[1] receive the parts' array checksums.
+static int build_parts(mpsp_csr* H, int L, int64_t n, const int64_t* rowptr, const int32_t* colidx,
+                       const uint32_t* limbs, const int32_t* exps, const uint8_t* signs,
+                       int64_t row_begin, int64_t row_end, uint32_t flags, bool dense,
+                       uint64_t* check) {
+  const int64_t nnz = rowptr[n];
   const int64_t nrows = row_end - row_begin;
   int rc = MPSP_OK;
-  // ---- part A: rows [rb, re)
   {
     std::vector<int64_t> lrp((size_t)nrows + 1);
     const int64_t k0 = rowptr[row_begin];
     for (int64_t r = 0; r <= nrows; ++r) lrp[(size_t)r] = rowptr[row_begin + r] - k0;
-    rc = build_part(H->A, L, nrows, lrp.data(), colidx + k0, nullptr, k0, limbs, exps, signs, dense);
+    rc = build_part(H->A, L, nrows, lrp.data(), colidx + k0, nullptr, k0, limbs, exps, signs, dense,
+                    check ? &check[0] : nullptr);
   }
-  // ---- a2: transpose (stable counting sort on column), rows [rb, re) of A^T
   if (rc == MPSP_OK && (flags & MPSP_WITH_TRANSPOSE)) {
     H->has_t = true;
     try {
@@ -568,11 +579,33 @@ static int create_impl(mpsp_csr** out, int p_bits, int64_t n, const int64_t* row
       std::vector<int64_t> lrp((size_t)nrows + 1);
       for (int64_t r = 0; r <= nrows; ++r) lrp[(size_t)r] = tcnt[(size_t)(row_begin + r)] - t0;
       rc = build_part(H->T, L, nrows, lrp.data(), tcol.data(), tsrc.data(), 0, limbs, exps, signs,
-                      dense);
+                      dense, check ? &check[1] : nullptr);
     } catch (const std::bad_alloc&) {
       rc = MPSP_E_NOMEM;
     }
   }
+  return rc;
+}
+
+static int create_impl(mpsp_csr** out, int p_bits, int64_t n, const int64_t* rowptr,
+                       const int32_t* colidx, const uint32_t* limbs, const int32_t* exps,
+                       const uint8_t* signs, int64_t row_begin, int64_t row_end, uint32_t flags,
+                       bool dense) {
+  if (!out) return MPSP_E_ARG;
+  *out = nullptr;
+  int rc = validate_csr(p_bits, n, rowptr, colidx, limbs, exps, signs, row_begin, row_end, flags);
+  if (rc) return rc;
+  const int L = p_bits / 32;
+  int dev = 0;
+  cudaError_t ce = cudaGetDevice(&dev);
+  if (ce != cudaSuccess) return cuda_fail(ce);
+  mpsp_csr* H = new (std::nothrow) mpsp_csr();
+  if (!H) return MPSP_E_NOMEM;
+  H->dev = dev; H->p = p_bits; H->L = L; H->n = n; H->rb = row_begin; H->re = row_end;
+  H->flags = flags;
+  H->dense = dense;
+  rc = build_parts(H, L, n, rowptr, colidx, limbs, exps, signs, row_begin, row_end, flags, dense,
+                   nullptr);
   if (rc == MPSP_OK && (H->A.nwrow > 0 || H->T.nwrow > 0)) {
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
@@ -590,6 +623,29 @@ static int create_impl(mpsp_csr** out, int p_bits, int64_t n, const int64_t* row
     return rc;
   }
   *out = H;
+  return MPSP_OK;
+}
+
+int mpsp_debug_host_build(int p_bits, int64_t n, const int64_t* rowptr, const int32_t* colidx,
+                          const uint32_t* limbs, const int32_t* exps, const uint8_t* signs,
+                          int64_t row_begin, int64_t row_end, uint32_t flags, int64_t out[12]) {
+  if (!out) return MPSP_E_ARG;
+  int rc = validate_csr(p_bits, n, rowptr, colidx, limbs, exps, signs, row_begin, row_end, flags);
+  if (rc) return rc;
+  mpsp_csr H;
+  uint64_t check[2] = {0, 0};
+  rc = build_parts(&H, p_bits / 32, n, rowptr, colidx, limbs, exps, signs, row_begin, row_end, flags,
+                   false, check);
+  if (rc) return rc;
+  const DevPart* ps[2] = {&H.A, &H.T};
+  for (int i = 0; i < 2; ++i) {
+    out[6 * i + 0] = ps[i]->nnz;
+    out[6 * i + 1] = ps[i]->nentries;
+    out[6 * i + 2] = ps[i]->nwrow;
+    out[6 * i + 3] = ps[i]->nslices;
+    out[6 * i + 4] = (int64_t)ps[i]->crow.size() - 1;
+    out[6 * i + 5] = (int64_t)check[i];
+  }
   return MPSP_OK;
 }
 
