@@ -421,14 +421,25 @@ int do_spmv(const mpsp_csr* A, bool transpose, const uint32_t* xl, const int32_t
   cudaStream_t us = (cudaStream_t)stream;
   cudaError_t ce;
   int err;
-  if (has_w && has_s && A->aux) {
-    // warp rows (the longest rows: the critical path) on the high-priority
-    // aux stream, short rows on the caller's stream; joined back there
+  // tuning knob MPSP_FORK (read per call): 1 (default) warp rows on the
+  // high-priority aux stream, 2 short rows there instead, 0 both in order on
+  // the caller's stream
+  static const int fork_mode = [] {
+    const char* v = std::getenv("MPSP_FORK");
+    return v ? std::atoi(v) : 1;
+  }();
+  if (has_w && has_s && A->aux && fork_mode != 0) {
+    // one kind of rows on the high-priority aux stream (default: the warp
+    // rows - the longest rows are the critical path), the other on the
+    // caller's stream; joined back there
+    const bool w_aux = fork_mode != 2;
     if ((ce = cudaEventRecord(A->ev_fork, us)) != cudaSuccess) return cuda_fail(ce);
     if ((ce = cudaStreamWaitEvent(A->aux, A->ev_fork, 0)) != cudaSuccess) return cuda_fail(ce);
-    if ((err = launch_spmv_long(L, pv, xv, yv, A->aux)) != 0) return cuda_fail((cudaError_t)err);
+    if ((err = w_aux ? launch_spmv_long(L, pv, xv, yv, A->aux) : launch_spmv(L, pv, xv, yv, A->aux)) != 0)
+      return cuda_fail((cudaError_t)err);
     if ((ce = cudaEventRecord(A->ev_join, A->aux)) != cudaSuccess) return cuda_fail(ce);
-    if ((err = launch_spmv(L, pv, xv, yv, stream)) != 0) return cuda_fail((cudaError_t)err);
+    if ((err = w_aux ? launch_spmv(L, pv, xv, yv, stream) : launch_spmv_long(L, pv, xv, yv, stream)) != 0)
+      return cuda_fail((cudaError_t)err);
     if ((ce = cudaStreamWaitEvent(us, A->ev_join, 0)) != cudaSuccess) return cuda_fail(ce);
     return MPSP_OK;
   }
