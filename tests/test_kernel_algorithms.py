@@ -109,7 +109,7 @@ def test_short_product_tie_is_never_certified():
 HB = 26
 
 
-def block_sum_chain(ts, p, G=32, ties_exact=False, transitions=False, stats=None):
+def block_sum_chain(ts, p, G=32, ties_exact=False, transitions=False, stats=None, herr2=False):
     """Model of spmv_wrow's chain over the products ts (oracle triples),
     G steps per block.  ties_exact=True models WChain::consume_u (spmv_wrow,
     G = 32U steps per warp pass), which sends a grid tie through the exact path
@@ -118,7 +118,12 @@ def block_sum_chain(ts, p, G=32, ties_exact=False, transitions=False, stats=None
     whose exact sum provably crosses 2^p (same signs) or provably drops to
     [2^(p-2), 2^(p-1)) (opposite signs) is rounded on the new grid directly
     (2u or u/2) from W's low bits and the step's fraction bits, without the
-    exact adder.  Returns (result, n_fast_steps)."""
+    exact adder.  herr2=True models WChain::consume as of round 2: the high
+    part of a step is taken from P = Y (plus sign) or ~Y (minus sign) - the
+    rounding / two's-complement carry is added later by the commit's carry
+    chain - so Q/H lies in [h, h + 2) and the bounds count two units of error
+    per step (the transitions' bounds widened by one unit).
+    Returns (result, n_fast_steps)."""
     L = p // 32
     S, E, sg, zero = 0, 0, 0, True         # exact S (grid integer), exponent, sign
     Shi, err, par = 0, 0, 0
@@ -165,6 +170,7 @@ def block_sum_chain(ts, p, G=32, ties_exact=False, transitions=False, stats=None
                 bad.append(tie and ties_exact)
             # tie parity, then signed Q, then the conservative checks
             p_run = par
+            PH = {}
             for k in range(len(blk)):
                 if not isinstance(Q[k], tuple):
                     continue
@@ -176,14 +182,20 @@ def block_sum_chain(ts, p, G=32, ties_exact=False, transitions=False, stats=None
                     p_run ^= (Y + inc) & 1
                 q = Y + inc
                 Q[k] = -q if neg else q
+                if herr2:
+                    PH[k] = hi(-Y - 1 if neg else Y)
+            EU = 2 if herr2 else 1               # bound error units per step
+
+            def hq(k):
+                return PH[k] if herr2 and k in PH else hi(Q[k])
             LB, cnt, fail = Shi, 0, None
             for k in range(len(blk)):
-                h = hi(Q[k])
+                h = hq(k)
                 act = k >= start and blk[k][1] != 0
                 if act:
-                    # the kernel bounds the floor errors before step k by k
+                    # the kernel bounds the floor errors before step k by EU k
                     ok = (not bad[k]) and LB + h - M1 >= (1 << (HB - 1)) and \
-                        LB + err + k + h + 1 <= (1 << HB)
+                        LB + err + EU * k + h + EU <= (1 << HB)
                     if not ok:
                         fail = k
                         break
@@ -191,7 +203,7 @@ def block_sum_chain(ts, p, G=32, ties_exact=False, transitions=False, stats=None
                 LB += h
             if fail is None:
                 S += sum(Q[start:])
-                Shi, err, par = LB, min(err + G, 1 << 28), p_run
+                Shi, err, par = LB, min(err + EU * G, 1 << 28), p_run
                 nfast += cnt
                 assert (1 << (p - 1)) <= S < (1 << p)
                 break
@@ -205,8 +217,8 @@ def block_sum_chain(ts, p, G=32, ties_exact=False, transitions=False, stats=None
                 # t's top 32 bits; W = S +- t/u is an integer (t is on a grid
                 # >= u) and RN(V) = RN_int(W / 2^k) on the grid 2^k u
                 dd = Et_ - E
-                LBf = Shi + sum(hi(q) for q in Q[start:fail])
-                ek = err + fail
+                LBf = Shi + sum(hq(k) for k in range(start, fail))
+                ek = err + EU * fail
                 mt = Mt_ >> (p - 32)
                 tl = mt << (dd - 6) if dd >= 6 else mt >> (6 - dd)
                 th = tl + ((1 << (dd - 6)) if dd >= 6 else 1)
@@ -231,9 +243,9 @@ def block_sum_chain(ts, p, G=32, ties_exact=False, transitions=False, stats=None
                     start = fail + 1
                     continue
             if transitions and not bad[fail]:
-                LBf = Shi + sum(hi(q) for q in Q[start:fail])
-                hf = hi(Q[fail])
-                ek = err + fail
+                LBf = Shi + sum(hq(k) for k in range(start, fail))
+                hf = hq(fail)
+                ek = err + EU * fail
                 st, Mt, Et = blk[fail]
                 d = min(E - Et, 32 * L + 32)
                 Y, rem = Mt >> d, Mt & ((1 << d) - 1)
@@ -243,7 +255,7 @@ def block_sum_chain(ts, p, G=32, ties_exact=False, transitions=False, stats=None
                     inc = (W & 1) & (1 if (rem != 0 or (W >> 1) & 1) else 0)
                     S = (W >> 1) + inc
                     E += 1
-                    Shi, err = (LBf + hf - 1) >> 1, ((ek + 3) >> 1) + 2
+                    Shi, err = (LBf + hf - 1) >> 1, ((ek + 2 + EU) >> 1) + 2
                     par = S & 1                                  # (the kernel reads it off R)
                     assert (1 << (p - 1)) <= S < (1 << p)
                     assert Shi <= hi(S) and hi(S) < Shi + err
@@ -251,7 +263,7 @@ def block_sum_chain(ts, p, G=32, ties_exact=False, transitions=False, stats=None
                         stats["up"] = stats.get("up", 0) + 1
                     start = fail + 1
                     continue
-                if st != sg and LBf + ek + hf + 2 <= LO and LBf + hf - M1 >= LO // 2:   # down: u/2
+                if st != sg and LBf + ek + hf + 1 + EU <= LO and LBf + hf - M1 >= LO // 2:   # down: u/2
                     b1 = (rem >> (d - 1)) & 1
                     b2 = (rem >> (d - 2)) & 1 if d >= 2 else 0
                     low = rem & ((1 << (d - 1)) - 1)
@@ -263,7 +275,7 @@ def block_sum_chain(ts, p, G=32, ties_exact=False, transitions=False, stats=None
                         up = (b2 == 0) or (tie2 and b1 == 0)
                         S = I - 1 + (1 if up else 0)
                     E -= 1
-                    Shi, err = 2 * (LBf + hf - M1) - 2, 2 * (ek + 2) + 4
+                    Shi, err = 2 * (LBf + hf - M1) - 2, 2 * (ek + 1 + EU) + 4
                     par = S & 1
                     assert (1 << (p - 1)) <= S < (1 << p)
                     assert Shi <= hi(S) and hi(S) < Shi + err
@@ -352,6 +364,8 @@ def test_block_sum_one_binade_transitions(p):
         got, _ = block_sum_chain(ts, p, G=rng.choice([4, 32]), transitions=True, ties_exact=True,
                                  stats=st)
         assert got == oracle_chain(ts, p), ("ties exact", trial)
+        got, _ = block_sum_chain(ts, p, transitions=True, herr2=True)   # round-2 consume
+        assert got == oracle_chain(ts, p), ("herr2", trial)
     assert st.get("up", 0) > 0 and st.get("down", 0) > 0
     assert 2 * (st.get("up", 0) + st.get("down", 0)) > st.get("exact", 0)
 
@@ -375,6 +389,8 @@ def test_block_sum_transitions_adversarial(p):
                 ts.append(_rand_t(rng, p, s_e - 3, s_e + 1))
         got, _ = block_sum_chain(ts, p, G=rng.choice([4, 32]), transitions=True)
         assert got == oracle_chain(ts, p), trial
+        got, _ = block_sum_chain(ts, p, transitions=True, herr2=True)
+        assert got == oracle_chain(ts, p), ("herr2", trial)
         # spmv_wrow's consume_u (64 steps per warp pass, grid ties sent to the
         # exact path, transitions on)
         got, _ = block_sum_chain(ts, p, G=64, transitions=True, ties_exact=True)
@@ -416,6 +432,8 @@ def test_block_sum_dominant_transitions(p):
         assert got == oracle_chain(ts, p), trial
         got, _ = block_sum_chain(ts, p, G=64, transitions=True, ties_exact=True)
         assert got == oracle_chain(ts, p), ("U=2", trial)
+        got, _ = block_sum_chain(ts, p, transitions=True, herr2=True)
+        assert got == oracle_chain(ts, p), ("herr2", trial)
     assert st.get("dom", 0) > 0
     # C4-like rows (products of values with exponents U[-32, 32]): the
     # dominant transition takes most of what used to be exact-path steps
