@@ -25,15 +25,6 @@
 
 namespace mpsp {
 
-// Warp rows (spmv_wrow): lane k of the row's warp owns the U = wrow_spl(L)
-// consecutive steps Uk .. Uk+U-1 of each 32U-step chunk.  Step j of such a
-// row (chunk c = j/(32U), q = j%(32U)) is stored at position c*32U +
-// 32(q%U) + q/U, so the warp's 32 loads of one u are consecutive entries.
-#ifndef MPSP_WU
-#define MPSP_WU 1
-#endif
-__host__ __device__ constexpr int wrow_spl(int L) { return L <= 8 ? MPSP_WU : 1; }
-
 struct PartView {
   const int64_t* slice_ptr;   // [nslices+1] entry offsets (multiples of 32)
   const int32_t* slot_row;    // [nslots]

@@ -196,7 +196,7 @@ int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32
     wptr[(size_t)i] = ew;
     wrow[(size_t)i] = r;
     wlen[(size_t)i] = (int32_t)(lrp[r + 1] - lrp[r]);
-    const int64_t cs = wide ? 1 : 32 * wrow_spl(L);
+    const int64_t cs = wide ? 1 : 32;
     ew += (wlen[(size_t)i] + cs - 1) / cs * cs;
   }
   // SELL slices of the remaining rows (chunk by chunk: a chunk's last slice
@@ -263,15 +263,7 @@ int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32
   parallel_for(nw, [&](int64_t i0, int64_t i1) {
     for (int64_t i = i0; i < i1; ++i) {
       const int32_t r = wrow[(size_t)i];
-      if (!wide) {                                // chunk-permuted (layout.h)
-        const int U = wrow_spl(L);
-        for (int64_t j = 0; j < wlen[(size_t)i]; ++j) {
-          const int64_t c = j / (32 * U), q = j % (32 * U);
-          put(wptr[(size_t)i] + c * 32 * U + 32 * (q % U) + q / U, lrp[r] + j);
-        }
-      } else {
-        for (int64_t j = 0; j < wlen[(size_t)i]; ++j) put(wptr[(size_t)i] + j, lrp[r] + j);
-      }
+      for (int64_t j = 0; j < wlen[(size_t)i]; ++j) put(wptr[(size_t)i] + j, lrp[r] + j);
     }
   });
   parallel_for(nslices, [&](int64_t s0, int64_t s1) {

@@ -292,11 +292,7 @@ template <int L>
 static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStream_t st) {
   const int64_t nshort = P.nslots;
   if (nshort <= 0) return 0;
-  // threads per block (env MPSP_SELL_TPB, read per launch): smaller blocks
-  // spread few warps more evenly over the SMs
-  const char* vt = std::getenv("MPSP_SELL_TPB");
-  const int tpb = vt ? std::atoi(vt) : 128;
-  const int threads = (tpb == 32 || tpb == 64) ? tpb : 128;
+  const int threads = 128;
   const int64_t blocks = (nshort + threads - 1) / threads;
   if constexpr (L == 32) {
     const char* vc = std::getenv("MPSP_CP");       // 0: register-prefetch kernel, 2: two stages
@@ -318,30 +314,6 @@ static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStrea
       return (int)cudaGetLastError();
     }
   }
-  if constexpr (L == 8 || L == 16) {
-    // MPSP_CPS=<minb> (tuning knob, 4..8): the one-stage cp.async kernel
-    const char* vs = std::getenv("MPSP_CPS");
-    if (vs && vs[0] >= '4' && vs[0] <= '8') {
-      constexpr int NC = L / 4;
-      const size_t smem = (size_t)3 * NC * CP_THREADS * 16;
-      static std::atomic<uint64_t> a4{0}, a5{0}, a6{0}, a8{0};
-      int e = 0;
-      const unsigned nb = (unsigned)blocks;
-      switch (vs[0]) {
-        case '4': e = ensure_smem_attr((const void*)spmv_sell_cp1<L, 4>, smem, a4);
-                  if (!e) spmv_sell_cp1<L, 4><<<nb, CP_THREADS, smem, st>>>(P, x, y); break;
-        case '5': e = ensure_smem_attr((const void*)spmv_sell_cp1<L, 5>, smem, a5);
-                  if (!e) spmv_sell_cp1<L, 5><<<nb, CP_THREADS, smem, st>>>(P, x, y); break;
-        case '6': e = ensure_smem_attr((const void*)spmv_sell_cp1<L, 6>, smem, a6);
-                  if (!e) spmv_sell_cp1<L, 6><<<nb, CP_THREADS, smem, st>>>(P, x, y); break;
-        default:  e = ensure_smem_attr((const void*)spmv_sell_cp1<L, 8>, smem, a8);
-                  if (!e) spmv_sell_cp1<L, 8><<<nb, CP_THREADS, smem, st>>>(P, x, y); break;
-      }
-      if (e) return e;
-      g_launches.fetch_add(1);
-      return (int)cudaGetLastError();
-    }
-  }
   // tuning knob (read per launch): MPSP_MINB = min resident blocks per SM
   // (register cap).  Defaults measured on B200: at L <= 8, 5 (96 registers,
   // no spills; C4 A x 0.380 -> 0.372 ms, A^T x 0.296 -> 0.279 ms) unless the
@@ -352,8 +324,7 @@ static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStrea
   int minb = L == 16 ? 4 : 1;
   if (L <= 8) {
     const int sms = current_sms();
-    const int64_t b128 = (nshort + 127) / 128;
-    minb = (b128 > (int64_t)sms * 5 && b128 <= (int64_t)sms * 6) ? 6 : 5;
+    minb = (blocks > (int64_t)sms * 5 && blocks <= (int64_t)sms * 6) ? 6 : 5;
   }
   if (vm) minb = std::atoi(vm);
   const unsigned nb = (unsigned)blocks;

@@ -14,8 +14,7 @@
 // parity of S_{k-1}; parities are prefix XORs of the Q_k's low bits and a tie
 // resets the parity to 0, so every lane gets its own in O(1) from two ballots.
 //
-// Per chunk of 32U entries (U consecutive steps per lane, wrow_spl(L) in
-// layout.h; the text below describes U = 1): each lane forms t_k = RN(a_k x_col)
+// Per block of 32 entries (one per lane): each lane forms t_k = RN(a_k x_col)
 // (Comba, IMAD.WIDE), aligns it to the grid u, and rounds it (Q_k).  A warp
 // scan of int32 high parts h_k = floor(Q_k/H) (H = 2^(p-26) grid units)
 // gives conservative bounds on every partial sum; if all are provably inside
@@ -56,11 +55,9 @@ struct WEntry {
   uint32_t sx;
 };
 
-// Step U*lane + u of chunk c: entry position e0 + c*32U + 32u + lane (the
-// chunk-permuted warp-row layout of layout.h: a warp's 32 loads of one u are
-// consecutive entries), i.e. offset `off` = c*32U + 32u from the lane's base
-// pointers (32-bit offsets, no 64-bit index arithmetic per step).  Invalid
-// steps (past the row end) load zero limbs.
+// Step 32c + lane of a warp row: entry position e0 + 32c + lane, i.e. offset
+// `off` = 32c from the lane's base pointers (32-bit offsets, no 64-bit index
+// arithmetic per step).  Invalid steps (past the row end) load zero limbs.
 template <int L>
 struct WRowBase {
   using CT = typename Chunk<L>::T;
@@ -98,77 +95,58 @@ __device__ __forceinline__ void wload(const WRowBase<L>& B, const XView& x, int 
 #define MPSP_WROW_MINB 4
 #endif
 // ---------------------------------------------------------------------------
-// spmv_wrow<L>: one warp per row; per chunk of 32U steps each lane forms the
-// products of its U consecutive steps (independent: ILP U) and the chain
-// advances by WChain::consume_u - one warp scan and one ballot per 32U steps.
-// Operands of chunk c+1 are loaded while chunk c is processed, its columns
-// one chunk earlier still.  DENSE (mpsp_dense_create): the column of step j
-// is j itself - no index array is read.
+// spmv_wrow<L>: one warp per row; per block of 32 steps each lane forms the
+// product of its step and the chain advances by WChain::consume.  Operands
+// of block c+1 are loaded while block c is processed, its columns one block
+// earlier still.  DENSE (mpsp_dense_create): the column of step j is j
+// itself - no index array is read.
 // ---------------------------------------------------------------------------
 template <int L, bool DENSE = false>
 __global__ void __launch_bounds__(128, (L <= 8 ? MPSP_WROW_MINB : 1)) spmv_wrow(PartView P, XView x, YView y) {
-  constexpr int U = wrow_spl(L);
-  constexpr int CS = 32 * U;
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= P.nwrow) return;
   const int64_t e0 = P.wrow_ptr[w];
   const int len = P.wrow_len[w];
   const int row = P.wrow_row[w];
-  const int nch = (len + CS - 1) / CS;
+  const int nb = (len + 31) / 32;
   WChain<L> ch;
   ch.init();
   WRowBase<L> B;
   B.init(P, e0, lane);
-  auto valid = [&](int c, int u) { return c * CS + U * lane + u < len; };
-  auto colof = [&](int c, int u) -> int {
-    if (!valid(c, u)) return 0;
-    if constexpr (DENSE) return c * CS + U * lane + u;
-    return __ldg(B.col + c * CS + 32 * u);
+  auto valid = [&](int c) { return 32 * c + lane < len; };
+  auto colof = [&](int c) -> int {
+    if (!valid(c)) return 0;
+    if constexpr (DENSE) return 32 * c + lane;
+    return __ldg(B.col + 32 * c);
   };
-  MP<L> t[U];
+  MP<L> t;
   if constexpr (L <= 16) {
-    // operands of chunk c+1 loaded while chunk c is processed (registers)
-    WEntry<L> nxt[U];
-    int cn[U];
-    if (nch > 0) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) wload<L>(B, x, 32 * u, valid(0, u), colof(0, u), nxt[u]);
-#pragma unroll
-      for (int u = 0; u < U; ++u) cn[u] = colof(1, u);
+    // operands of block c+1 loaded while block c is processed (registers)
+    WEntry<L> nxt;
+    int cn = 0;
+    if (nb > 0) {
+      wload<L>(B, x, 0, valid(0), colof(0), nxt);
+      cn = colof(1);
     }
-    for (int c = 0; c < nch; ++c) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const WEntry<L> cur = nxt[u];
-        if (c + 1 < nch) {
-          wload<L>(B, x, (c + 1) * CS + 32 * u, valid(c + 1, u), cn[u], nxt[u]);
-          cn[u] = colof(c + 2, u);
-        }
-        mul_entry<L>(cur.a, cur.w, cur.x, cur.ex, cur.sx, t[u]);
+    for (int c = 0; c < nb; ++c) {
+      const WEntry<L> cur = nxt;
+      if (c + 1 < nb) {
+        wload<L>(B, x, 32 * (c + 1), valid(c + 1), cn, nxt);
+        cn = colof(c + 2);
       }
-      if constexpr (U == 1)
-        ch.consume(t[0], lane);          // ties resolved from the running parity
-      else
-        ch.template consume_u<U>(t, lane);
+      mul_entry<L>(cur.a, cur.w, cur.x, cur.ex, cur.sx, t);
+      ch.consume(t, lane);
     }
   } else {
     // L = 32: no register prefetch (the operands alone are 64 registers)
-    int cn[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) cn[u] = nch > 0 ? colof(0, u) : 0;
-    for (int c = 0; c < nch; ++c) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        WEntry<L> cur;
-        wload<L>(B, x, c * CS + 32 * u, valid(c, u), cn[u], cur);
-        cn[u] = colof(c + 1, u);
-        mul_entry<L>(cur.a, cur.w, cur.x, cur.ex, cur.sx, t[u]);
-      }
-      if constexpr (U == 1)
-        ch.consume(t[0], lane);          // ties resolved from the running parity
-      else
-        ch.template consume_u<U>(t, lane);
+    int cn = nb > 0 ? colof(0) : 0;
+    for (int c = 0; c < nb; ++c) {
+      WEntry<L> cur;
+      wload<L>(B, x, 32 * c, valid(c), cn, cur);
+      cn = colof(c + 1);
+      mul_entry<L>(cur.a, cur.w, cur.x, cur.ex, cur.sx, t);
+      ch.consume(t, lane);
     }
   }
   MP<L> s;

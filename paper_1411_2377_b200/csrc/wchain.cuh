@@ -370,100 +370,6 @@ struct WChain {
     mp_add<L>(s, tf);
     reset_to(s, lane);
   }
-
-  // s := the chain over this warp's 32U products, lane k holding the U
-  // consecutive steps Uk .. Uk+U-1 in t[0..U-1] (zero limbs: no step).  One
-  // warp scan and one ballot per 32U steps; the U alignments of a lane are
-  // independent.  A grid tie is sent to step_f (exact path) instead of being
-  // resolved from the running parity (rare on the configs; the stress corpus
-  // forces it).
-  template <int U>
-  __device__ __forceinline__ void consume_u(const MP<L> (&t)[U], int lane) {
-    constexpr unsigned FULL = 0xffffffffu;
-    constexpr int32_t LO = 1 << (HB - 1), HI = 1 << HB;
-    constexpr int CS = 32 * U;
-    bool tz[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) tz[u] = t[u].is_zero();
-    int start = 0;
-    while (start < CS) {
-      if (szero) {
-        int fu = U;
-#pragma unroll
-        for (int u = U - 1; u >= 0; --u)
-          if (!tz[u] && U * lane + u >= start) fu = u;
-        const unsigned nzm = __ballot_sync(FULL, fu < U);
-        if (nzm == 0u) break;
-        const int kf = __ffs(nzm) - 1;
-        const int uf = __shfl_sync(FULL, fu, kf);
-        MP<L> tf;
-        pick<U>(t, uf, tf);
-#pragma unroll
-        for (int i = 0; i < L; ++i) tf.m[i] = __shfl_sync(FULL, tf.m[i], kf);
-        tf.e = __shfl_sync(FULL, tf.e, kf);
-        tf.s = __shfl_sync(FULL, tf.s, kf);
-        reset_to(tf, lane);
-        start = U * kf + uf + 1;
-        continue;
-      }
-      uint32_t Q[U][N];
-      int32_t h[U], Hx[U];
-      bool bad[U];
-      int32_t tot = 0;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const bool act = (U * lane + u >= start) && !tz[u];
-        align_q<L>(t[u], act, E, sg, Q[u], h[u], bad[u]);
-        Hx[u] = tot;
-        tot += h[u];
-      }
-      int32_t Pi = tot;                               // inclusive scan of the lane totals
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int32_t v = __shfl_up_sync(FULL, Pi, o);
-        if (lane >= o) Pi += v;
-      }
-      const int32_t X = Shi + Pi - tot;               // S/H before this lane's first step >= X
-      int fu = U;
-#pragma unroll
-      for (int u = U - 1; u >= 0; --u) {
-        const bool act = (U * lane + u >= start) && !tz[u];
-        const int32_t LB = X + Hx[u];
-        const int32_t ek = err + U * lane + u;
-        const bool ok = !act || (!bad[u] && LB + h[u] - 1 >= LO && LB + ek + h[u] + 1 <= HI);
-        if (!ok) fu = u;
-      }
-      const unsigned failM = __ballot_sync(FULL, fu < U);
-      if (failM == 0u) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) add_n<N>(R, R, Q[u]);
-        Shi += __shfl_sync(FULL, Pi, 31);
-        err = min(err + CS, 1 << 28);                 // saturates: checks then fail
-        break;
-      }
-      const int kf = __ffs(failM) - 1;
-      const int uf = __shfl_sync(FULL, fu, kf);
-      int32_t LBl = 0, hl = 0;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (lane < kf || (lane == kf && u < uf)) add_n<N>(R, R, Q[u]);   // steps before f
-        if (u == uf) { LBl = X + Hx[u]; hl = h[u]; }
-      }
-      MP<L> tu;
-      pick<U>(t, uf, tu);
-      step_f(tu, kf, __shfl_sync(FULL, LBl, kf), __shfl_sync(FULL, hl, kf), err + U * kf + uf, lane);
-      start = U * kf + uf + 1;
-    }
-  }
-
-  // t[uf] for a warp-uniform runtime index uf (no dynamic register indexing)
-  template <int U>
-  __device__ __forceinline__ static void pick(const MP<L> (&t)[U], int uf, MP<L>& o) {
-    o = t[0];
-#pragma unroll
-    for (int u = 1; u < U; ++u)
-      if (u == uf) o = t[u];
-  }
 };
 
 }  // namespace mpsp

@@ -161,8 +161,7 @@ def test_tie_prone_rows(p, thr, monkeypatch):
 
 @pytest.fixture
 def all_rows_warp(monkeypatch):
-    """Route every nonempty row through the warp-row kernel (U steps per lane,
-    layout.h wrow_spl: chunks of 64 steps at p <= 256, 32 above)."""
+    """Route every nonempty row through the warp-row kernel (32-step blocks)."""
     monkeypatch.setenv("MPSP_LONG_T", "0")
 
 
@@ -181,7 +180,7 @@ def test_warp_kernel_tie_prone(p, all_rows_warp):
 
 @pytest.mark.parametrize("thr", ["0", "31", "63", "100", "300"])
 def test_warp_threshold_split_c4(thr, monkeypatch):
-    """Row lengths around the 32- and 64-step chunk boundaries, ragged tails."""
+    """Row lengths around the 32- and 64-step block boundaries, ragged tails."""
     monkeypatch.setenv("MPSP_LONG_T", thr)
     d = gen.make("C4", n=20_000, seed=10)
     for op in ("ax", "atx"):

@@ -111,9 +111,9 @@ HB = 26
 
 def block_sum_chain(ts, p, G=32, ties_exact=False, transitions=False, stats=None, herr2=False):
     """Model of spmv_wrow's chain over the products ts (oracle triples),
-    G steps per block.  ties_exact=True models WChain::consume_u (spmv_wrow,
-    G = 32U steps per warp pass), which sends a grid tie through the exact path
-    instead of resolving its parity.
+    G steps per block.  ties_exact=True models a chain that sends a grid tie
+    through the exact path instead of resolving its parity (the U-steps-per-
+    lane variant measured in round 2, G = 32U).
     transitions=True models WChain's one-binade transitions: a failing step
     whose exact sum provably crosses 2^p (same signs) or provably drops to
     [2^(p-2), 2^(p-1)) (opposite signs) is rounded on the new grid directly
@@ -391,8 +391,8 @@ def test_block_sum_transitions_adversarial(p):
         assert got == oracle_chain(ts, p), trial
         got, _ = block_sum_chain(ts, p, transitions=True, herr2=True)
         assert got == oracle_chain(ts, p), ("herr2", trial)
-        # spmv_wrow's consume_u (64 steps per warp pass, grid ties sent to the
-        # exact path, transitions on)
+        # 64 steps per warp pass, grid ties sent to the exact path,
+        # transitions on (the U = 2 variant)
         got, _ = block_sum_chain(ts, p, G=64, transitions=True, ties_exact=True)
         assert got == oracle_chain(ts, p), ("U=2", trial)
 
