@@ -123,8 +123,13 @@ __device__ __forceinline__ void add3w(uint32_t& a0, uint32_t& a1, uint32_t& a2, 
 #ifndef MPSP_NCH8
 #define MPSP_NCH8 1
 #endif
+#ifndef MPSP_NCH16
+#define MPSP_NCH16 MPSP_NCH
+#endif
 template <int L>
-struct MulChains { static constexpr int n = L >= 16 ? MPSP_NCH : (L >= 4 ? MPSP_NCH8 : 1); };
+struct MulChains {
+  static constexpr int n = L >= 32 ? MPSP_NCH : (L >= 16 ? MPSP_NCH16 : (L >= 4 ? MPSP_NCH8 : 1));
+};
 
 // --------------------------------------------------------------------------
 // t = RN_p(a * x).  a, x: L-limb mantissas (zero allowed: result zero).
