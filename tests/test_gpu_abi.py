@@ -365,3 +365,74 @@ def test_row_chunks_device_and_host_pipeline(cfg, n, op, chunks, monkeypatch):
         f(*hx, out=hy)
         assert_same(hy, want, f"host pinned chunks={chunks}")
     A.close()
+
+
+@pytest.mark.parametrize("cfg,n,op,G", [("C5", 4900, "ax", 2), ("C5", 4900, "ax", 4),
+                                        ("C2", 5000, "atx", 3), ("C3", 3000, "ax", 2)])
+def test_distcsr_apply_emulated_ranks(cfg, n, op, G, monkeypatch):
+    """DistCSR itself for G ranks emulated in one process on one GPU: each
+    rank's object (interior / boundary row-range handles, apply() ordering:
+    interior kernels launched before finish(), boundary kernels after, output
+    slices) is built with the rank / world size patched in and an exchange
+    stand-in that fills the needed window at finish() and junk before - so an
+    interior kernel that read outside the own block, or a boundary kernel run
+    before the exchange, would show.  Concatenated blocks vs the oracle."""
+    import torch
+    from paper_1411_2377_b200 import MPVec
+    from paper_1411_2377_b200 import dist as D
+    d = gen.make(cfg, n=n, seed=23)
+    n = d["n"]
+    tr = op == "atx"
+    want = oracle_full(d, op)
+    L = d["p"] // 32
+    xfull = MPVec.from_host(d["x_limbs"], d["x_exps"], d["x_signs"], device="cuda:0")
+
+    class FakeX:
+        def __init__(self, n_, L_, window, group=None, device=None, mode="auto", packer=None):
+            self.rb, self.re = D.block_range(n_, G, rank[0])
+            self.win = window
+            self.mode, self.bytes_in = "window", 0
+            g = torch.Generator(device="cpu").manual_seed(rank[0])
+            junk = torch.randint(-2 ** 31, 2 ** 31 - 1, (n_, L_), generator=g, dtype=torch.int32)
+            junk[:, -1] |= -2 ** 31                     # normalised junk
+            self.x = MPVec(junk.cuda(), torch.zeros(n_, dtype=torch.int32, device="cuda"),
+                           torch.zeros(n_, dtype=torch.uint8, device="cuda"))
+
+        def local_view(self):
+            return MPVec(self.x.limbs[self.rb:self.re], self.x.exps[self.rb:self.re],
+                         self.x.signs[self.rb:self.re])
+
+        def start(self, stream=None):
+            return []
+
+        def finish(self, works, stream=None):
+            lo, hi = self.win
+            for dst, src in ((self.x.limbs, xfull.limbs), (self.x.exps, xfull.exps),
+                             (self.x.signs, xfull.signs)):
+                dst[lo:hi].copy_(src[lo:hi])
+            return self.x
+
+        def close(self):
+            pass
+
+    rank = [0]
+    monkeypatch.setattr(D, "XExchange", FakeX)
+    monkeypatch.setattr(D.dist, "get_world_size", lambda group=None: G)
+    monkeypatch.setattr(D.dist, "get_rank", lambda group=None: rank[0])
+    monkeypatch.setattr(D.dist, "get_backend", lambda group=None: "nccl")
+    parts, inner = [], 0
+    for r in range(G):
+        rank[0] = r
+        Dc = D.DistCSR(d["p"], d["rowptr"], d["colidx"], d["limbs"], d["exps"], d["signs"],
+                       transpose=tr, device="cuda:0")
+        rb, re = Dc.rows
+        xl = MPVec(xfull.limbs[rb:re].clone(), xfull.exps[rb:re].clone(), xfull.signs[rb:re].clone())
+        y = Dc.apply(xl, transpose=tr)
+        torch.cuda.synchronize()
+        parts.append(y.to_host())
+        inner += Dc.interior_rows(tr)
+        Dc.close()
+    cat = tuple(np.concatenate([p_[i] for p_ in parts]) for i in range(3))
+    assert_same(cat, want, f"DistCSR {cfg} G={G} {op}")
+    if cfg in ("C5", "C2"):
+        assert inner > n // 2
