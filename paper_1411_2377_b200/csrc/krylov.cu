@@ -151,6 +151,40 @@ __device__ __forceinline__ void load_prod(const DotWork& W, int64_t blk, int lan
   t.s = P[(L + 1) * 32 + lane];
 }
 
+// Exclusive prefix of the segments' fp64 sums, in place (one block of 1024
+// threads, O(nseg)): the guess of each segment's starting binade.  Only
+// estimates - a wrong guess just makes a segment fail validation.
+__global__ void __launch_bounds__(1024) dot_prefix(double* segsum, int64_t nseg, const int* stop) {
+  if (stop && *stop) return;
+  __shared__ double part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (nseg + 1023) / 1024;
+  const int64_t a = (int64_t)t * per, b = min(nseg, a + per);
+  double acc = 0.0;
+  for (int64_t k = a; k < b; ++k) acc += segsum[k];
+  part[t] = acc;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {            // inclusive Hillis-Steele scan
+    const double v = t >= o ? part[t - o] : 0.0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  double run = t > 0 ? part[t - 1] : 0.0;
+  for (int64_t k = a; k < b; ++k) {
+    const double v = segsum[k];
+    segsum[k] = run;
+    run += v;
+  }
+}
+
+int launch_dot_prefix(double* segsum, int64_t nseg, const int* stop, void* stream) {
+  if (nseg <= 0) return 0;
+  dot_prefix<<<1, 1024, 0, (cudaStream_t)stream>>>(segsum, nseg, stop);
+  launch_counter_add(1);
+  return (int)cudaGetLastError();
+}
+
 template <int L>
 __global__ void __launch_bounds__(128) dot_speculate(DotWork W, int64_t nseg, const int* stop) {
   if (stop && *stop) return;
@@ -159,10 +193,7 @@ __global__ void __launch_bounds__(128) dot_speculate(DotWork W, int64_t nseg, co
   const int64_t seg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (seg >= nseg || seg == 0) return;
-  double pre = 0.0;                                // fp64 prefix of the segment sums
-  for (int64_t j = lane; j < seg; j += 32) pre += W.segsum[j];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(FULL, pre, o);
+  const double pre = W.segsum[seg];                // fp64 prefix (dot_prefix)
   int e2 = 0;
   const double f = frexp(fabs(pre), &e2);
   bool valid = (pre != 0.0) && isfinite(pre) && f > 0.0;
@@ -229,12 +260,13 @@ __global__ void __launch_bounds__(32) dot_chain(int64_t n, DotWork W, int64_t ns
   WChain<L> ch;
   ch.init();
   // (block b+1's products are loaded while block b is consumed: the lone
-  // chain warp would otherwise wait a full memory latency per block)
-  auto sequential = [&](int64_t seg) {
+  // chain warp would otherwise wait a full memory latency per block; the
+  // first block of a segment to walk is loaded by the caller, before the
+  // commits of the segments ahead of it)
+  auto sequential = [&](int64_t seg, MP<L>& first) {
     if (lane == 0) atomicAdd(&g_dot_stats[0], 1ull);
     const int64_t b0 = seg * DSEG_NB;
-    MP<L> t, tn;
-    if (b0 * 32 < n) load_prod<L>(W, b0, lane, tn);
+    MP<L> t, tn = first;
     for (int b = 0; b < DSEG_NB; ++b) {
       const int64_t blk = b0 + b;
       if (blk * 32 >= n) break;
@@ -243,16 +275,57 @@ __global__ void __launch_bounds__(32) dot_chain(int64_t n, DotWork W, int64_t ns
       ch.consume(t, lane);
     }
   };
-  int64_t s = 0;
-  while (s < nseg) {
-    if (s == 0 || ch.szero) {
-      sequential(s);
-      ++s;
+  auto first_of = [&](int64_t seg, MP<L>& t) {
+    if (seg * DSEG_NB * 32 < n) load_prod<L>(W, seg * DSEG_NB, lane, t);
+    else t.set_zero();
+  };
+  // The window of 32 segments [base, base+32): lane j holds segment base+j's
+  // speculation record.  After committing f segments and walking segment
+  // base+f, the records of base+f+1 .. base+31 move down by f+1 lanes and
+  // only the tail is loaded - issued before the walk, so its latency hides
+  // behind it.
+  int64_t base = 0;
+  int wv = 0;
+  int32_t weg = 0;
+  uint32_t wsg = 0u;
+  long long wmn = 0, wmx = 0, wht = 0;
+  auto load_rec = [&](int64_t jj) {
+    const bool in = jj < nseg;
+    wv = in ? W.valid[jj] : 0;
+    weg = in ? W.eg[jj] : 0;
+    wsg = in ? W.sg[jj] : 0u;
+    wmn = in ? W.minv[jj] : 0;
+    wmx = in ? W.maxv[jj] : 0;
+    wht = in ? W.htot[jj] : 0;
+  };
+  {
+    MP<L> t0;
+    first_of(0, t0);
+    sequential(0, t0);                          // segment 0 starts from +0
+    base = 1;
+    load_rec(base + lane);
+  }
+  while (base < nseg) {
+    if (ch.szero) {                             // the chain is exactly zero: walk
+      MP<L> t0;
+      first_of(base, t0);
+      sequential(base, t0);
+      const int sh = 1;
+      const int64_t jn = base + lane + sh;
+      // shift the window down by one lane, load the new tail
+      const int v2 = __shfl_down_sync(FULL, wv, sh);
+      const int32_t e2 = __shfl_down_sync(FULL, weg, sh);
+      const uint32_t s2 = __shfl_down_sync(FULL, wsg, sh);
+      const long long m1 = __shfl_down_sync(FULL, wmn, sh), m2 = __shfl_down_sync(FULL, wmx, sh);
+      const long long h2 = __shfl_down_sync(FULL, wht, sh);
+      if (lane < 32 - sh) { wv = v2; weg = e2; wsg = s2; wmn = m1; wmx = m2; wht = h2; }
+      else load_rec(jn);
+      base += sh;
       continue;
     }
-    const int64_t j = s + lane;
+    const int64_t j = base + lane;
     const bool in = j < nseg;
-    const long long ht = in ? W.htot[j] : 0;
+    const long long ht = in ? wht : 0;
     const long long cn = DSEG;
     long long hi = ht, ci = cn;                     // inclusive scans
 #pragma unroll
@@ -262,11 +335,14 @@ __global__ void __launch_bounds__(32) dot_chain(int64_t n, DotWork W, int64_t ns
       if (lane >= o) { hi += x; ci += y; }
     }
     const long long hpre = hi - ht, cpre = ci - cn;
-    bool ok = in && W.valid[j] && W.eg[j] == ch.E && W.sg[j] == ch.sg;
-    ok = ok && ((long long)ch.Shi + hpre + W.minv[j] - 1 >= LO) &&
-         ((long long)ch.Shi + hpre + (long long)ch.err + cpre + W.maxv[j] + 1 <= HI);
+    bool ok = in && wv && weg == ch.E && wsg == ch.sg;
+    ok = ok && ((long long)ch.Shi + hpre + wmn - 1 >= LO) &&
+         ((long long)ch.Shi + hpre + (long long)ch.err + cpre + wmx + 1 <= HI);
     const unsigned failM = __ballot_sync(FULL, !ok);
     const int f = failM ? __ffs(failM) - 1 : 32;
+    const bool walk = f < 32 && base + f < nseg;
+    MP<L> t0;
+    if (walk) first_of(base + f, t0);              // in flight during the commits
     if (f > 0) {
       if (lane == 0) atomicAdd(&g_dot_stats[1], (unsigned long long)f);
       if (lane < f) {
@@ -277,12 +353,21 @@ __global__ void __launch_bounds__(32) dot_chain(int64_t n, DotWork W, int64_t ns
       }
       ch.Shi = (int32_t)((long long)ch.Shi + __shfl_sync(FULL, hi, f - 1));
       ch.err = (int32_t)min((long long)ch.err + __shfl_sync(FULL, ci, f - 1), 1ll << 28);
-      s += f;
     }
-    if (f < 32 && s < nseg) {
-      sequential(s);
-      ++s;
+    // next window: base + f + 1 (after the walk of base + f) or base + 32
+    const int sh = walk ? f + 1 : 32;
+    {
+      const int src = min(lane + sh, 31);
+      const int v2 = __shfl_sync(FULL, wv, src);
+      const int32_t e2 = __shfl_sync(FULL, weg, src);
+      const uint32_t s2 = __shfl_sync(FULL, wsg, src);
+      const long long m1 = __shfl_sync(FULL, wmn, src), m2 = __shfl_sync(FULL, wmx, src);
+      const long long h2 = __shfl_sync(FULL, wht, src);
+      if (lane + sh < 32) { wv = v2; weg = e2; wsg = s2; wmn = m1; wmx = m2; wht = h2; }
+      else load_rec(base + lane + sh);              // issued before the walk
     }
+    if (walk) sequential(base + f, t0);
+    base += sh;
   }
   MP<L> r;
   ch.exact(r);
@@ -581,9 +666,10 @@ struct KrylovOps {
     DotWork W = carve(work, nseg);
     const unsigned nb = (unsigned)((nseg * 32 + 127) / 128);
     dot_products<L><<<nb, 128, 0, st>>>(n, u, v, W, nseg, stop);
+    dot_prefix<<<1, 1024, 0, st>>>(W.segsum, nseg, stop);
     dot_speculate<L><<<nb, 128, 0, st>>>(W, nseg, stop);
     dot_chain<L><<<1, 32, 0, st>>>(n, W, nseg, out, stop);
-    launch_counter_add(3);
+    launch_counter_add(4);
     return (int)cudaGetLastError();
   }
   static size_t bytes(int64_t n) {

@@ -388,10 +388,7 @@ __global__ void __launch_bounds__(32 * KW) wseg_speculate(int64_t n, int64_t nse
   const int64_t seg = (int64_t)blockIdx.x * KW + warp;
   if (seg >= nseg || seg == 0) return;
   uint32_t* sm = wsm + warp * 8 * L;               // 2L + 34 words used
-  double pre = 0.0;
-  for (int64_t j = lane; j < seg; j += 32) pre += G.segsum[j];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(FULL, pre, o);
+  const double pre = G.segsum[seg];               // fp64 prefix (launch_dot_prefix)
   int e2 = 0;
   frexp(fabs(pre), &e2);
   bool valid = pre != 0.0 && isfinite(pre);
@@ -713,6 +710,7 @@ struct WideOps {
       const int64_t blocks = std::min<int64_t>((n + KW - 1) / KW, 148 * 16);
       wdot_products<K><<<(unsigned)blocks, 32 * KW, KW * SM, st>>>(n, u, v, P, G.fp, stop);
       wseg_sums<K><<<(unsigned)((nseg * 32 + 127) / 128), 128, 0, st>>>(n, nseg, G, stop);
+      if ((e = launch_dot_prefix(G.segsum, nseg, stop, st))) return e;
       if ((e = attr(wseg_speculate<K>, KW * SM))) return e;
       wseg_speculate<K><<<(unsigned)((nseg + KW - 1) / KW), 32 * KW, KW * SM, st>>>(n, nseg, Pin, G, stop);
       launch_counter_add(3);
