@@ -324,7 +324,9 @@ def roofline(meta, nrows, nnz, kern_s, int_peak, hbm_peak, peak_src, skip=0.0):
     if t_int >= t_mem:
         r = {"bound": "alu", "achieved": macs / kern_s / 1e12, "peak": int_peak / 1e12,
              "unit": "Tlimb-MAC/s",
-             "peak_source": "mpsp_imad_bench: measured sustained Comba IMAD.WIDE rate, this run"}
+             "peak_source": "mpsp_imad_bench: measured sustained limb-MAC rate, this run, the "
+                            "faster of the Comba (IMAD.WIDE) and operand-scanning (IMAD + IMAD.HI) "
+                            "forms, per-lane operands"}
     else:
         r = {"bound": "hbm", "achieved": bytes_ / kern_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
              "peak_source": peak_src}

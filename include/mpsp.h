@@ -285,13 +285,16 @@ int mpsp_debug_dot_stats(unsigned long long out[2]);
 
 /*
  * mpsp_imad_bench - measures the sustained 32x32->64 limb-MAC rate of the
- * current device with the same Comba (product-scanning) instruction pattern
- * the SpMV kernels use (IMAD.WIDE.U32 with carry-out), all SMs busy.
- *   out[0] = limb-MACs per second, out[1] = kernel seconds, out[2] = SM count.
- * The roofline denominator for the integer-bound configurations.
- * Errors: MPSP_E_CUDA.
+ * current device, all SMs busy, per-lane operands, in two instruction forms:
+ * the Comba (product-scanning) pattern the SpMV kernels use (IMAD.WIDE.U32
+ * with carry-out) and operand scanning (IMAD + IMAD.HI with carry chains).
+ *   out[0] = limb-MACs per second of the faster form (the peak),
+ *   out[1] = its kernel seconds, out[2] = SM count,
+ *   out[3] = Comba limb-MACs per second, out[4] = operand-scanning rate.
+ * out[0] is the roofline denominator for the integer-bound configurations.
+ * Errors: MPSP_E_ARG (out NULL), MPSP_E_CUDA.
  */
-int mpsp_imad_bench(double out[3]);
+int mpsp_imad_bench(double out[5]);
 
 /* Supported precisions query: returns 1 if p_bits is supported, else 0. */
 int mpsp_supported_precision(int p_bits);

@@ -117,9 +117,10 @@ def launch_count() -> int:
 
 
 def imad_bench() -> dict:
-    out = (ctypes.c_double * 3)()
+    out = (ctypes.c_double * 5)()
     check(lib().mpsp_imad_bench(out), "mpsp_imad_bench")
-    return {"limb_macs_per_s": out[0], "seconds": out[1], "sms": int(out[2])}
+    return {"limb_macs_per_s": out[0], "seconds": out[1], "sms": int(out[2]),
+            "comba_limb_macs_per_s": out[3], "operand_scan_limb_macs_per_s": out[4]}
 
 
 def supported_precision(p: int) -> bool:

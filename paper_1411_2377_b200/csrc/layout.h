@@ -103,7 +103,7 @@ int launch_vec_pack(int L, bool unpack, int64_t count, const uint32_t* limbs_in,
                     uint32_t* rec_out, uint32_t* limbs_out, int32_t* exps_out, uint8_t* signs_out,
                     void* stream);
 // Integer-MAC microbenchmark (roofline denominator); returns cudaError_t.
-int run_imad_bench(double out[3]);
+int run_imad_bench(double out[5]);
 // Launches this process has made.
 int64_t launch_counter_get();
 

@@ -1274,7 +1274,7 @@ int mpsp_debug_dot_stats(unsigned long long out[2]) {
   return e ? cuda_fail((cudaError_t)e) : MPSP_OK;
 }
 
-int mpsp_imad_bench(double out[3]) {
+int mpsp_imad_bench(double out[5]) {
   if (!out) return MPSP_E_ARG;
   int e = run_imad_bench(out);
   if (e != 0) return cuda_fail((cudaError_t)e);

@@ -355,31 +355,61 @@ int launch_spmv(int L, const PartView& P, const XView& x, const YView& y, void* 
 }
 
 // --------------------------------------------------------------------------
-// Integer limb-MAC microbenchmark (roofline denominator).
-// Each thread runs an 8x8-limb Comba product per iteration (64 limb-MACs,
-// same mac3 pattern as mp_mul) and folds the high half back into its
-// operand so nothing is dead code.
+// Integer limb-MAC microbenchmarks (roofline denominator).
+// Each thread runs an 8x8-limb product per iteration (64 limb-MACs) with
+// per-lane operands and folds the high half back into its operand so nothing
+// is dead code.  Two instruction forms of the same 32x32->64 MAC:
+//   COMBA (product scanning, the kernels' mac3): one IMAD.WIDE.U32 with
+//     carry-out on the FMA-heavy pipe + ~0.5 IADD3.X per limb-MAC;
+//   OPERAND scanning: per row a_i * x a carry chain of low words and one of
+//     high words: IMAD + IMAD.HI on the FMA pipes + IADD3.X on the ALU pipe.
+// The peak reported is the faster of the two (B200: operand scanning, ~36 vs
+// ~28 limb-MACs/clk/SM); inside the SpMV kernels operand scanning measured
+// slower (the adder needs the ALU pipe the carries would take), DESIGN.md.
 // --------------------------------------------------------------------------
 constexpr int IB_L = 8;
+template <bool OS>
 __global__ void __launch_bounds__(256) imad_bench_kernel(uint32_t* out, int iters, uint32_t seed) {
   uint32_t a[IB_L], b[IB_L];
 #pragma unroll
   for (int i = 0; i < IB_L; ++i) {
     a[i] = seed * (threadIdx.x + 1) + i * 0x9E3779B9u;
-    b[i] = (seed ^ blockIdx.x) * 0x85EBCA6Bu + i;
+    b[i] = (seed ^ blockIdx.x) * 0x85EBCA6Bu + i * threadIdx.x;   // per lane
   }
   for (int it = 0; it < iters; ++it) {
-    uint32_t c0 = 0u, c1 = 0u, c2 = 0u, r[IB_L];
+    uint32_t r[IB_L];
+    if constexpr (!OS) {
+      uint32_t c0 = 0u, c1 = 0u, c2 = 0u;
 #pragma unroll
-    for (int k = 0; k < 2 * IB_L - 1; ++k) {
+      for (int k = 0; k < 2 * IB_L - 1; ++k) {
+#pragma unroll
+        for (int i = 0; i < IB_L; ++i) {
+          const int j = k - i;
+          if (j < 0 || j >= IB_L) continue;
+          mac3(c0, c1, c2, a[i], b[j]);
+        }
+        if (k >= IB_L - 1) r[k - (IB_L - 1)] = c0;
+        c0 = c1; c1 = c2; c2 = 0u;
+      }
+    } else {
+      uint32_t q[2 * IB_L];
+#pragma unroll
+      for (int i = 0; i < 2 * IB_L; ++i) q[i] = 0u;
 #pragma unroll
       for (int i = 0; i < IB_L; ++i) {
-        const int j = k - i;
-        if (j < 0 || j >= IB_L) continue;
-        mac3(c0, c1, c2, a[i], b[j]);
+        asm volatile("mad.lo.cc.u32 %0, %1, %2, %0;" : "+r"(q[i]) : "r"(a[i]), "r"(b[0]));
+#pragma unroll
+        for (int j = 1; j < IB_L; ++j)
+          asm volatile("madc.lo.cc.u32 %0, %1, %2, %0;" : "+r"(q[i + j]) : "r"(a[i]), "r"(b[j]));
+        asm volatile("addc.u32 %0, %0, 0;" : "+r"(q[i + IB_L]));
+        asm volatile("mad.hi.cc.u32 %0, %1, %2, %0;" : "+r"(q[i + 1]) : "r"(a[i]), "r"(b[0]));
+#pragma unroll
+        for (int j = 1; j < IB_L; ++j)
+          asm volatile("madc.hi.cc.u32 %0, %1, %2, %0;" : "+r"(q[i + j + 1]) : "r"(a[i]), "r"(b[j]));
+        if (i + IB_L + 1 < 2 * IB_L) asm volatile("addc.u32 %0, %0, 0;" : "+r"(q[i + IB_L + 1]));
       }
-      if (k >= IB_L - 1) r[k - (IB_L - 1)] = c0;
-      c0 = c1; c1 = c2; c2 = 0u;
+#pragma unroll
+      for (int i = 0; i < IB_L; ++i) r[i] = q[i + IB_L];
     }
 #pragma unroll
     for (int i = 0; i < IB_L; ++i) a[i] ^= r[i];
@@ -387,10 +417,28 @@ __global__ void __launch_bounds__(256) imad_bench_kernel(uint32_t* out, int iter
   uint32_t acc = 0u;
 #pragma unroll
   for (int i = 0; i < IB_L; ++i) acc ^= a[i];
-  if (acc == 0x12345678u) out[blockIdx.x] = acc;  // practically never; keeps work live
+  if (acc == seed + 0x12345678u) out[blockIdx.x] = acc;  // practically never; keeps work live
 }
 
-int run_imad_bench(double out[3]) {
+template <bool OS>
+static cudaError_t time_imad(uint32_t* d_out, int blocks, int threads, int iters, float& ms) {
+  imad_bench_kernel<OS><<<blocks, threads>>>(d_out, 16, 1u);  // warm-up
+  g_launches.fetch_add(1);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  imad_bench_kernel<OS><<<blocks, threads>>>(d_out, iters, 7u);
+  g_launches.fetch_add(1);
+  cudaEventRecord(e1);
+  const cudaError_t e = cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return e;
+}
+
+int run_imad_bench(double out[5]) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -398,26 +446,18 @@ int run_imad_bench(double out[3]) {
   cudaError_t e = cudaMalloc(&d_out, 4096 * sizeof(uint32_t));
   if (e != cudaSuccess) return (int)e;
   const int blocks = sms * 8, threads = 256, iters = 4096;
-  imad_bench_kernel<<<blocks, threads>>>(d_out, 16, 1u);  // warm-up
-  g_launches.fetch_add(1);
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  cudaEventRecord(e0);
-  imad_bench_kernel<<<blocks, threads>>>(d_out, iters, 7u);
-  g_launches.fetch_add(1);
-  cudaEventRecord(e1);
-  e = cudaEventSynchronize(e1);
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
+  float ms_c = 0.f, ms_o = 0.f;
+  e = time_imad<false>(d_out, blocks, threads, iters, ms_c);
+  if (e == cudaSuccess) e = time_imad<true>(d_out, blocks, threads, iters, ms_o);
   cudaFree(d_out);
   if (e != cudaSuccess) return (int)e;
   const double macs = (double)blocks * threads * iters * IB_L * IB_L;
-  out[0] = macs / (ms * 1e-3);
-  out[1] = ms * 1e-3;
+  const double rc = macs / (ms_c * 1e-3), ro = macs / (ms_o * 1e-3);
+  out[0] = rc > ro ? rc : ro;
+  out[1] = (rc > ro ? ms_c : ms_o) * 1e-3;
   out[2] = sms;
+  out[3] = rc;
+  out[4] = ro;
   return (int)cudaGetLastError();
 }
 

@@ -118,14 +118,23 @@ struct WChain {
     s.s = sg;
   }
 
-  // s := the chain over this warp's 32 products t (lane k holds step k)
-  __device__ __forceinline__ void consume(const MP<L>& t, int lane) {
+  // s := the chain over this warp's 32 products t (lane k holds step k).
+  // Clobbers t: the steps a pass has disposed of (lanes <= f) are zeroed
+  // before the next pass, so "act" is just t != 0 and the aligned product
+  // needs no lane mask (padding lanes hold zero limbs already).
+  __device__ __forceinline__ void consume(MP<L>& t, int lane) {
     constexpr unsigned FULL = 0xffffffffu;
     constexpr int32_t LO = 1 << (HB - 1), HI = 1 << HB;
     const unsigned below = (1u << lane) - 1u;
-    const bool tz = t.is_zero();       // padding lanes have zero limbs
     int start = 0;
+    auto retire = [&](int f) {          // steps 0..f are done
+      if (lane <= f) {
+#pragma unroll
+        for (int i = 0; i < L; ++i) t.m[i] = 0u;
+      }
+    };
     while (start < 32) {
+      const bool tz = t.is_zero();
       if (szero) {
         // s = +0: the first nonzero product is absorbed exactly
         const unsigned nzm = __ballot_sync(FULL, !tz && lane >= start);
@@ -137,10 +146,11 @@ struct WChain {
         tf.e = __shfl_sync(FULL, t.e, f);
         tf.s = __shfl_sync(FULL, t.s, f);
         reset_to(tf, lane);
+        retire(f);
         start = f + 1;
         continue;
       }
-      const bool act = (lane >= start) && !tz;
+      const bool act = !tz;
       const int32_t d32 = sub_sat(E, t.e);            // E - t.e, saturated to int32
       const bool badd = act && d32 < 1;              // |t| >= 2^(E-1): leaves the binade
       const bool use = act && !badd;
@@ -177,11 +187,14 @@ struct WChain {
       // is taken from P, so Q/H lies in [h, h + 2): the bounds below count
       // two units of error per step.
       const uint32_t neg = (use && t.s != sg) ? 1u : 0u;
-      const uint32_t nm = 0u - neg, um = use ? ~0u : 0u;
+      // (Y of a lane that leaves the binade - badd - is not masked: such a
+      // lane fails, so neither its Q nor its h reach a committed step or a
+      // bound of one, and step_f reads hf only for a lane that is "use")
+      const uint32_t nm = 0u - neg;
       const uint32_t cin = use ? (neg ? 1u - inc : inc) : 0u;
       uint32_t Q[N];
 #pragma unroll
-      for (int i = 0; i < L; ++i) Q[i] = (Y[i + 1] & um) ^ nm;
+      for (int i = 0; i < L; ++i) Q[i] = Y[i + 1] ^ nm;
       Q[L] = nm;
       Q[L + 1] = nm;
       const int32_t h = hi_of_q<L>(Q);
@@ -205,6 +218,7 @@ struct WChain {
       const int f = __ffs(failM) - 1;
       if (lane < f) add_n_cin<N>(R, R, Q, cin);      // steps before f are valid
       step_f(t, f, __shfl_sync(FULL, LB, f), __shfl_sync(FULL, h, f), err + 2 * f, lane);
+      retire(f);
       start = f + 1;
     }
   }
