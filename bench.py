@@ -81,11 +81,12 @@ def algorithmic(meta, nrows, nnz=None):
 
 def executed_macs_per_nnz(L):
     """Limb-MACs the kernels execute per nnz: the short
-    product with an exactness certificate forms L^2 - (L-3)(L-2)/2 at L >= 4;
-    p > 1024 (spmv_wide) the hi columns plus three lo columns, L^2/2 + 19L."""
+    product with an exactness certificate forms L^2 - (L-2)(L-1)/2 at L >= 4
+    (columns L-2 .. 2L-2); p > 1024 (spmv_wide) the hi columns plus three lo
+    columns, L^2/2 + 19L."""
     if L > 32:
         return L * L // 2 + 19 * L
-    return L * L - (L - 3) * (L - 2) // 2 if L >= 4 else L * L
+    return L * L - (L - 2) * (L - 1) // 2 if L >= 4 else L * L
 
 
 class ClockSampler:

@@ -235,24 +235,36 @@ __device__ __forceinline__ uint32_t comba_lower(const uint32_t (&a)[L], const ui
 
 // --------------------------------------------------------------------------
 // t = RN_p(a * x) by a SHORT product with an exactness certificate (DESIGN.md
-// "Product").  Only columns k >= K0 = L-3 are formed first (T); the omitted
-// part N = sum_{i+j<K0} a_i x_j 2^(32(i+j)) satisfies 0 <= N < 2^B,
-// B = 32(L-2)+5 (K0 < 32 terms per column, each < 2^64).  Let W be the bits
-// of T in [B, round bit).  If W is neither all zeros nor all ones, adding N
-// cannot carry past W, so every bit from the round bit up - hence the
-// normalisation, the kept limbs and the round bit - is the exact product's,
-// and the sticky is 1 (W or W+1 is nonzero).  Otherwise (probability ~2^-56
-// on random mantissas; common only for structured inputs) the lower columns
-// are formed too and their carry added in: the exact product.
-// Executed limb-MACs on the fast path: L^2 - (L-3)(L-2)/2 (L=32: 618 of 1024).
+// "Product").  Only columns k >= K0 = L-D are formed first (T, zero carry-in;
+// D = MPSP_SHORT_D = 2 by default); the omitted part
+// N = sum_{i+j<K0} a_i x_j 2^(32(i+j)) satisfies 0 <= N < 2^B, B = 32 K0 + 37
+// (fewer than 32 terms per column, each < 2^64).  Let W be the bits of T in
+// [B, round bit).  If W is neither all zeros nor all ones, adding N cannot
+// carry past W, so every bit from the round bit up - hence the normalisation,
+// the kept limbs and the round bit - is the exact product's, and the sticky
+// is 1 (W or W+1 is nonzero).  Otherwise the lower columns are formed too and
+// their carry added in: the exact product.  W has 25 bits at D = 2 (57 at
+// D = 3), so random mantissas take that path with probability ~2^-24 (a few
+// products per 10^8); structured inputs whose operand has zero low limbs take
+// the exact-short path below instead.
+// Executed limb-MACs on the fast path: L^2 - (L-D)(L-D+1)/2
+// (D = 2, L = 8 / 16 / 32: 43 / 151 / 588; D = 3: 49 / 165 / 618).
 // --------------------------------------------------------------------------
-// The rounding half of mp_mul: T = comba_upper<L, L-3>(a, x) (limbs L-3 ..
-// 2L-1 of the product's upper columns) -> t.  Split out so a caller can
-// form T for the next entry in the same basic block as other work.
+#ifndef MPSP_SHORT_D
+#define MPSP_SHORT_D 2
+#endif
+template <int L>
+struct Short {
+  static constexpr int D = MPSP_SHORT_D;   // columns L-D .. 2L-2 are formed
+  static constexpr int K0 = L - D;
+  static constexpr int NT = L + D;         // T[m] = limb K0 + m, m in [0, L+D)
+};
+
+// The rounding half of mp_mul: T = comba_upper<L, K0>(a, x) -> t.
 template <int L>
 __device__ __forceinline__ void mp_mul_finish(const uint32_t (&a)[L], int32_t ea, uint32_t sa,
                                               const uint32_t (&x)[L], int32_t ex, uint32_t sx,
-                                              uint32_t (&T)[L + 3], MP<L>& t);
+                                              uint32_t (&T)[Short<L>::NT], MP<L>& t);
 
 template <int L>
 __device__ __forceinline__ void mp_mul(const uint32_t (&a)[L], int32_t ea, uint32_t sa,
@@ -261,8 +273,8 @@ __device__ __forceinline__ void mp_mul(const uint32_t (&a)[L], int32_t ea, uint3
   if constexpr (L < 4) {
     mp_mul_full<L>(a, ea, sa, x, ex, sx, t);
   } else {
-    uint32_t T[L + 3];                               // limbs L-3 .. 2L-1
-    comba_upper<L, L - 3>(a, x, T);
+    uint32_t T[Short<L>::NT];                        // limbs K0 .. 2L-1
+    comba_upper<L, Short<L>::K0>(a, x, T);
     mp_mul_finish<L>(a, ea, sa, x, ex, sx, T, t);
   }
 }
@@ -270,49 +282,62 @@ __device__ __forceinline__ void mp_mul(const uint32_t (&a)[L], int32_t ea, uint3
 template <int L>
 __device__ __forceinline__ void mp_mul_finish(const uint32_t (&a)[L], int32_t ea, uint32_t sa,
                                               const uint32_t (&x)[L], int32_t ex, uint32_t sx,
-                                              uint32_t (&T)[L + 3], MP<L>& t) {
-  {
-    constexpr int K0 = L - 3;
-    uint32_t sh = (~T[L + 2]) >> 31;                 // top product bit clear -> 1
-    const uint32_t wmask = (1u << (31u - sh)) - 1u;  // T[2] bits below the round bit
+                                              uint32_t (&T)[Short<L>::NT], MP<L>& t) {
+  constexpr int D = Short<L>::D, K0 = Short<L>::K0, NT = Short<L>::NT;
+  static_assert(D == 2 || D == 3, "short product: D in {2, 3}");
+  uint32_t sh = (~T[NT - 1]) >> 31;                // top product bit clear -> 1
+  // W: the bits between B (bit 5 of T[1]) and the round bit (bit 31 - sh of
+  // T[D-1], the product's limb L-1)
+  bool amb;
+  if constexpr (D == 3) {
+    const uint32_t wmask = (1u << (31u - sh)) - 1u;
     const uint32_t w1 = T[1] >> 5, w2 = T[2] & wmask;
-    const bool amb = ((w1 | w2) == 0u) | ((w1 == 0x07FFFFFFu) & (w2 == wmask));
-    const bool zero = (a[L - 1] == 0u) | (x[L - 1] == 0u);
-    uint32_t stk = 1u;
-    // Exact short product: every omitted term a_i x_j (i + j < K0) has i, j
-    // < K0, so N = 0 when either operand's limbs 0 .. K0-1 are all zero
-    // (e.g. a power-of-two mantissa: C5's diagonal 4, exact-integer data) -
-    // then T is the exact product and no lower column is formed.
-    bool low0 = false;
-    if (amb && !zero) {
-      uint32_t ao = 0u, xo = 0u;
+    amb = ((w1 | w2) == 0u) | ((w1 == 0x07FFFFFFu) & (w2 == wmask));
+  } else {
+    const uint32_t wv = ((T[1] << sh) << 1) >> 7;  // bits 6 .. 30 of T[1] << sh
+    amb = (wv == 0u) | (wv == 0x01FFFFFFu);
+  }
+  const bool zero = (a[L - 1] == 0u) | (x[L - 1] == 0u);
+  uint32_t stk = 1u;
+  auto low_sticky = [&]() {                        // T's bits below the round bit
+    uint32_t v = (T[D - 1] << sh) << 1;
 #pragma unroll
-      for (int i = 0; i < K0; ++i) { ao |= a[i]; xo |= x[i]; }
-      low0 = (ao == 0u) | (xo == 0u);
-      if (low0) stk = T[0] | T[1] | ((T[2] << sh) << 1);
-    }
-    if (amb && !zero && !low0) {                     // rare: complete the product
-      uint32_t c0, c1, c2;
-      const uint32_t slo = comba_lower<L, K0>(a, x, c0, c1, c2);
-      uint32_t C[L + 3];
-      C[0] = c0; C[1] = c1; C[2] = c2;
+    for (int i = 0; i < D - 1; ++i) v |= T[i];
+    return v;
+  };
+  // Exact short product: every omitted term a_i x_j (i + j < K0) has i, j
+  // < K0, so N = 0 when either operand's limbs 0 .. K0-1 are all zero
+  // (e.g. a power-of-two mantissa: C5's diagonal 4, exact-integer data) -
+  // then T is the exact product and no lower column is formed.
+  bool low0 = false;
+  if (amb && !zero) {
+    uint32_t ao = 0u, xo = 0u;
 #pragma unroll
-      for (int i = 3; i < L + 3; ++i) C[i] = 0u;
-      add_n<L + 3>(T, T, C);
-      sh = (~T[L + 2]) >> 31;
-      stk = slo | T[0] | T[1] | ((T[2] << sh) << 1);
-    }
+    for (int i = 0; i < K0; ++i) { ao |= a[i]; xo |= x[i]; }
+    low0 = (ao == 0u) | (xo == 0u);
+    if (low0) stk = low_sticky();
+  }
+  if (amb && !zero && !low0) {                     // rare: complete the product
+    uint32_t c0, c1, c2;
+    const uint32_t slo = comba_lower<L, K0>(a, x, c0, c1, c2);
+    uint32_t C[NT];
+    C[0] = c0; C[1] = c1; C[2] = c2;
 #pragma unroll
-    for (int i = L - 1; i >= 0; --i) t.m[i] = __funnelshift_l(T[i + 2], T[i + 3], sh);
-    const uint32_t rb = (T[2] << sh) >> 31;
-    const uint32_t cy = rne_increment<L>(t.m, rb, stk);
-    if (cy) t.m[L - 1] = 0x80000000u;
-    t.e = ea + ex - (int32_t)sh + (int32_t)cy;
-    t.s = sa ^ sx;
-    if (zero) {
+    for (int i = 3; i < NT; ++i) C[i] = 0u;
+    add_n<NT>(T, T, C);
+    sh = (~T[NT - 1]) >> 31;
+    stk = slo | low_sticky();
+  }
 #pragma unroll
-      for (int i = 0; i < L; ++i) t.m[i] = 0u;
-    }
+  for (int i = L - 1; i >= 0; --i) t.m[i] = __funnelshift_l(T[i + D - 1], T[i + D], sh);
+  const uint32_t rb = (T[D - 1] << sh) >> 31;
+  const uint32_t cy = rne_increment<L>(t.m, rb, stk);
+  if (cy) t.m[L - 1] = 0x80000000u;
+  t.e = ea + ex - (int32_t)sh + (int32_t)cy;
+  t.s = sa ^ sx;
+  if (zero) {
+#pragma unroll
+    for (int i = 0; i < L; ++i) t.m[i] = 0u;
   }
 }
 

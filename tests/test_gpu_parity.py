@@ -224,3 +224,36 @@ def test_power_of_two_entries(p):
              limbs=limbs, exps=exps, signs=signs, x_limbs=xl, x_exps=xe, x_signs=xs)
     for op in ("ax", "atx"):
         assert_same(gpu_run(d, op), oracle_full(d, op), f"pow2 p={p} {op}")
+
+
+@pytest.mark.parametrize("op", ["ax", "atx"])
+@pytest.mark.parametrize("p", [128, 256, 512, 1024])
+def test_short_product_ambiguous_window(p, op):
+    """Products whose certificate window (the bits of the upper columns
+    between the bound on the omitted low columns and the round bit: bits
+    p-27 .. p-3 of x when a = 2^(p-1) + 1) is all zeros or all ones, with a
+    nonzero low limb in both operands: the kernels must form the full
+    product.  a x = x 2^(p-1) + x, so the window is x's own bits there."""
+    import random
+    rng = random.Random(p)
+    L = p // 32
+    n, per_row = 64, 6
+    vals, cols, rowptr = [], [], [0]
+    xs = []
+    for i in range(n):
+        M = (1 << (p - 1)) | rng.getrandbits(p - 1)
+        win = ((1 << 25) - 1) << (p - 27)
+        M = (M & ~win) | (win if i % 2 else 0) | 1          # window all 0 / all 1, low bit set
+        xs.append((rng.getrandbits(1), M, rng.randint(-8, 8)))
+    for r in range(n):
+        cs = sorted(rng.sample(range(n), per_row))
+        for c in cs:
+            Ma = (1 << (p - 1)) + 1 if rng.random() < 0.7 else (1 << (p - 1)) | rng.getrandbits(p - 1)
+            vals.append((rng.getrandbits(1), Ma, rng.randint(-8, 8)))
+            cols.append(c)
+        rowptr.append(len(cols))
+    al, ae, as_ = gen.pack_triples(vals, p)
+    xl, xe, xsg = gen.pack_triples(xs, p)
+    d = dict(p=p, n=n, rowptr=np.array(rowptr, np.int64), colidx=np.array(cols, np.int32),
+             limbs=al, exps=ae, signs=as_, x_limbs=xl, x_exps=xe, x_signs=xsg)
+    assert_same(gpu_run(d, op), oracle_full(d, op), f"ambiguous window p={p} {op}")

@@ -26,21 +26,27 @@ M32 = (1 << 32) - 1
 
 
 # ---------------------------------------------------------------- 1. product
-def short_product(Ma, Mx, p):
+def short_product(Ma, Mx, p, D=None):
     """Model of mp_mul: returns (M, dE, certified) or None when the
-    certificate fails (the kernel then forms the full product)."""
+    certificate fails (the kernel then forms the full product).  Columns
+    k >= K0 = L - D are formed: D = 2 in mp_mul (L <= 32, MPSP_SHORT_D), 3 in
+    the warp form for L = 64..256 (wide_mp.cuh wmul)."""
     L = p // 32
+    if D is None:
+        D = 2 if L <= 32 else 3
     a = [(Ma >> (32 * i)) & M32 for i in range(L)]
     x = [(Mx >> (32 * i)) & M32 for i in range(L)]
-    K0 = L - 3
+    K0 = L - D
     T = sum(a[i] * x[j] << (32 * (i + j)) for i in range(L) for j in range(L) if i + j >= K0)
     N = Ma * Mx - T
-    # K0 < 32 terms per omitted column (L <= 32, mp_mul): +5; the warp form
-    # for L = 64..256 (wide_mp.cuh wmul) has K0 < 256 terms: +8
-    B = 32 * (L - 2) + (5 if L <= 32 else 8)
+    # K0 < 32 terms per omitted column (L <= 32, mp_mul): +37 over column K0;
+    # the warp form for L = 64..256 has K0 < 256 terms: +40
+    B = 32 * K0 + (37 if L <= 32 else 40)
     assert 0 <= N < (1 << B)                      # the bound the certificate uses
     sh = 0 if (T >> (64 * L - 1)) & 1 else 1
     rpos = 32 * L - 1 - sh                        # round bit position
+    if D == 2:
+        B += 1 - sh                               # the kernel's window: bits 6..30 of T[1] << sh
     W = (T >> B) & ((1 << (rpos - B)) - 1)
     if W == 0 or W == (1 << (rpos - B)) - 1:
         return None
@@ -54,14 +60,15 @@ def short_product(Ma, Mx, p):
     return q, dE
 
 
-@pytest.mark.parametrize("p", [128, 256, 512, 1024, 2048, 8192])
-def test_short_product_certificate_random(p):
+@pytest.mark.parametrize("p,D", [(128, 2), (256, 2), (512, 2), (1024, 2), (256, 3), (1024, 3),
+                                 (2048, 3), (8192, 3)])
+def test_short_product_certificate_random(p, D):
     rng = random.Random(p)
     hits = 0
     for _ in range(3000 if p <= 1024 else 300):
         Ma = (1 << (p - 1)) | rng.getrandbits(p - 1)
         Mx = (1 << (p - 1)) | rng.getrandbits(p - 1)
-        r = short_product(Ma, Mx, p)
+        r = short_product(Ma, Mx, p, D)
         if r is None:
             continue
         hits += 1
@@ -70,8 +77,8 @@ def test_short_product_certificate_random(p):
     assert hits == (3000 if p <= 1024 else 300)   # random mantissas never need the full product
 
 
-@pytest.mark.parametrize("p", [128, 256, 512, 2048])
-def test_short_product_certificate_adversarial(p):
+@pytest.mark.parametrize("p,D", [(128, 2), (256, 2), (512, 2), (256, 3), (2048, 3)])
+def test_short_product_certificate_adversarial(p, D):
     """Structured mantissas (powers of two, all-ones runs, carries rippling
     into the round bit, exact ties): whenever the certificate passes the
     result is exact; ambiguous cases must be rejected, never mis-rounded."""
@@ -87,7 +94,7 @@ def test_short_product_certificate_adversarial(p):
     rejected = 0
     for Ma in corpus:
         for Mx in corpus[:60]:
-            r = short_product(Ma, Mx, p)
+            r = short_product(Ma, Mx, p, D)
             s, M, E = oracle.mul((0, Ma, 0), (0, Mx, 0), p)
             if r is None:
                 rejected += 1
@@ -446,16 +453,16 @@ def test_block_sum_dominant_transitions(p):
     assert st.get("dom", 0) > 2 * st.get("exact", 0)
 
 
-@pytest.mark.parametrize("p", [128, 256, 1024])
-def test_short_product_zero_low_limbs_is_exact(p):
-    """mp_mul's exact case: when either operand's limbs 0 .. K0-1 (K0 = L-3)
+@pytest.mark.parametrize("p,D", [(128, 2), (256, 2), (1024, 2), (256, 3), (1024, 3)])
+def test_short_product_zero_low_limbs_is_exact(p, D):
+    """mp_mul's exact case: when either operand's limbs 0 .. K0-1 (K0 = L-D)
     are all zero, every omitted Comba term a_i x_j (i + j < K0) is zero, so
     the upper columns T are the exact product and rounding T directly (round
     bit and sticky read from T) equals RN(a*x) - e.g. C5's diagonal 4
     (M = 2^(p-1)), whose products the certificate cannot decide (all-zero
     bits below the round bit)."""
     L = p // 32
-    K0 = L - 3
+    K0 = L - D
     rng = random.Random(p + 99)
     for _ in range(400):
         hi_bits = 32 * (L - K0)
