@@ -434,13 +434,11 @@ __device__ __forceinline__ uint32_t add_n_cin(uint32_t (&z)[N], const uint32_t (
 template <int L>
 __device__ __forceinline__ void mp_add(MP<L>& s, const MP<L>& t) {
   const bool tz = t.is_zero(), sz = s.is_zero();
-  // |M_s| < |M_t| matters only for equal exponents: the top limbs decide it
-  // unless they are equal too (rare: then the full borrow chain, warp-uniform)
-  uint32_t mlt = s.m[L - 1] < t.m[L - 1] ? 1u : 0u;
-  if constexpr (L > 1) {
-    if (__any_sync(__activemask(), (t.e == s.e) & (s.m[L - 1] == t.m[L - 1])))
-      mlt = lt_n<L>(s.m, t.m);
-  }
+  // |M_s| < |M_t| matters only for equal exponents: the top limbs decide it.
+  // When they are equal too, s is taken as the big operand; if that was the
+  // smaller one and the signs differ, Z - Y borrows (its top limbs cancel,
+  // so >= 32 bits cancel): the rare branch below negates it.
+  const uint32_t mlt = s.m[L - 1] < t.m[L - 1] ? 1u : 0u;
   // bitwise (not short-circuit) logic: no branches in the common path
   const bool t_big = !tz & (sz | (t.e > s.e) | ((t.e == s.e) & (mlt != 0u)));
   const int32_t eb = t_big ? t.e : s.e;
@@ -463,17 +461,26 @@ __device__ __forceinline__ void mp_add(MP<L>& s, const MP<L>& t) {
 #pragma unroll
   for (int i = 0; i <= L; ++i) Y[i] ^= msk;
   const uint32_t cin = sub & (stk == 0u ? 1u : 0u);
-  const uint32_t W = add_n_cin<L + 1>(Z, Z, Y, cin) & (sub ^ 1u);
+  const uint32_t c = add_n_cin<L + 1>(Z, Z, Y, cin);
+  const uint32_t W = c & (sub ^ 1u);
+  const bool neg = (sub != 0u) & (c == 0u);             // Z - Y < 0 (see above)
   stk |= Z[0] & W;                                      // bit lost by the right shift
 #pragma unroll
   for (int i = 0; i < L; ++i) Z[i] = __funnelshift_r(Z[i], Z[i + 1], W);
   Z[L] = __funnelshift_r(Z[L], W, W);
   uint32_t lz = __clz(Z[L]);
-  if (lz < 32u) {
+  uint32_t sres = sb;
+  if ((lz < 32u) & !neg) {
 #pragma unroll
     for (int i = L; i > 0; --i) Z[i] = __funnelshift_l(Z[i - 1], Z[i], lz);
     Z[0] <<= lz;
   } else {            // >= 32 bits cancelled, or an exact zero (rare)
+    if (neg) {        // d = 0: nothing reached the sticky, -Z is exact
+#pragma unroll
+      for (int i = 0; i <= L; ++i) Z[i] = ~Z[i];
+      inc_n<L + 1>(Z, 1u);
+      sres ^= 1u;
+    }
     lz = clz_limbs<L + 1>(Z);
     shl_bits<L + 1>(Z, lz);
   }
@@ -485,7 +492,7 @@ __device__ __forceinline__ void mp_add(MP<L>& s, const MP<L>& t) {
   const uint32_t cy = rne_increment<L>(s.m, rb, st);
   if (cy) s.m[L - 1] = 0x80000000u;
   s.e = e + (int32_t)cy;
-  s.s = sb;
+  s.s = sres;
 }
 
 }  // namespace mpsp

@@ -257,3 +257,41 @@ def test_short_product_ambiguous_window(p, op):
     d = dict(p=p, n=n, rowptr=np.array(rowptr, np.int64), colidx=np.array(cols, np.int32),
              limbs=al, exps=ae, signs=as_, x_limbs=xl, x_exps=xe, x_signs=xsg)
     assert_same(gpu_run(d, op), oracle_full(d, op), f"ambiguous window p={p} {op}")
+
+
+@pytest.mark.parametrize("p", [64, 128, 256, 512, 1024])
+def test_equal_top_limb_cancellation(p):
+    """Adds of opposite signs whose exponents and top limbs are equal: the
+    adder orders the operands by the top limbs only, so when the accumulator
+    is the smaller one the difference borrows and must be negated (>= 32 bits
+    cancel).  Products are the A entries themselves (x = 1), the pair sits in
+    the middle of a row, both orders, the differing limb anywhere below the
+    top one."""
+    import random
+    rng = random.Random(p + 5)
+    L = p // 32
+    top = 1 << (p - 1)
+    one = (0, top, 1)                                   # x = 1
+    vals, rowptr = [], [0]
+    for _ in range(96):
+        M = top | rng.getrandbits(p - 1)
+        k = rng.randrange(0, L - 1) if L > 1 else 0     # limb below the top that differs
+        M2 = M ^ (rng.getrandbits(32) << (32 * k)) | (M & (0xFFFFFFFF << (32 * (L - 1))))
+        M2 = (M2 & ~(0xFFFFFFFF << (32 * (L - 1)))) | (M & (0xFFFFFFFF << (32 * (L - 1))))
+        if M2 == M:
+            M2 = M ^ 1
+        e = rng.randint(-6, 6)
+        sa = rng.getrandbits(1)
+        row = [(rng.getrandbits(1), top | rng.getrandbits(p - 1), e - rng.randint(40, 300)),
+               (sa, M, e), (1 - sa, M2, e),
+               (rng.getrandbits(1), top | rng.getrandbits(p - 1), e - rng.randint(1, 90))]
+        vals += row
+        rowptr.append(len(vals))
+    n = len(rowptr) - 1
+    cols = [j % 4 for j in range(len(vals))]            # distinct columns, ascending
+    al, ae, as_ = gen.pack_triples(vals, p)
+    xl, xe, xsg = gen.pack_triples([one] * max(n, 4), p)
+    d = dict(p=p, n=max(n, 4), rowptr=np.array(rowptr + [rowptr[-1]] * (max(n, 4) - n), np.int64),
+             colidx=np.array(cols, np.int32), limbs=al, exps=ae, signs=as_,
+             x_limbs=xl, x_exps=xe, x_signs=xsg)
+    assert_same(gpu_run(d, "ax"), oracle_full(d, "ax"), f"equal top limbs p={p}")
