@@ -83,7 +83,7 @@ __device__ __forceinline__ uint32_t expw_sign(int32_t w) { return (uint32_t)w >>
 // branch; C5's diagonal 4 sits at the same step of every interior row).  The
 // test reads the loaded limbs (an OR over L-1 limbs, ~L/3 instructions; at
 // L = 16 it measured 8% slower on C3, whose entries are never powers of two).
-template <int L>
+template <int L, bool FW = false>
 __device__ __forceinline__ void mul_entry(const uint32_t (&a)[L], int32_t w, const uint32_t (&x)[L],
                                           int32_t ex, uint32_t sx, MP<L>& t) {
   const int32_t ea = expw_exp(w);
@@ -92,7 +92,7 @@ __device__ __forceinline__ void mul_entry(const uint32_t (&a)[L], int32_t w, con
     uint32_t lo = 0u;
 #pragma unroll
     for (int i = 0; i < L - 1; ++i) lo |= a[i];
-    if (__all_sync(__activemask(), (lo == 0u) & (a[L - 1] == 0x80000000u))) {
+    if (__all_sync(FW ? 0xffffffffu : __activemask(), (lo == 0u) & (a[L - 1] == 0x80000000u))) {
       // a = 2^(ea-1): a x = M_x 2^(ex + ea - 1 - p), exact
       const bool xz = x[L - 1] == 0u;
 #pragma unroll

@@ -345,7 +345,9 @@ __device__ __forceinline__ void mp_mul_finish(const uint32_t (&a)[L], int32_t ea
 // Variable shifts over N-limb register arrays (binary decomposition of the
 // limb count so indices stay compile-time; no local memory).
 // --------------------------------------------------------------------------
-template <int N>
+// FW: every lane of the warp executes the call (full-warp collectives, no
+// __activemask()); otherwise the active lanes'
+template <int N, bool FW = false>
 __device__ __forceinline__ void shr_bits_sticky(uint32_t (&v)[N], uint32_t d, uint32_t& sticky) {
   const uint32_t q = d >> 5, r = d & 31u;
   // limb steps only up to the largest limb shift any active lane needs
@@ -354,7 +356,7 @@ __device__ __forceinline__ void shr_bits_sticky(uint32_t (&v)[N], uint32_t d, ui
   // warp needs there, run unconditionally (a branch per level made ptxas copy
   // the whole array at each merge; measured C4 -2%, C5 needs neither)
   constexpr int UNC = N <= 17 ? 4 : 1;
-  const uint32_t qmax = N > UNC ? __reduce_max_sync(__activemask(), q) : 0u;
+  const uint32_t qmax = N > UNC ? __reduce_max_sync(FW ? 0xffffffffu : __activemask(), q) : 0u;
 #pragma unroll
   for (int b = 1; b <= N; b <<= 1) {
     if (b < UNC || qmax >= (uint32_t)b) {
@@ -431,7 +433,7 @@ __device__ __forceinline__ uint32_t add_n_cin(uint32_t (&z)[N], const uint32_t (
 //   the cancellation at d <= 1; >= 32 bits of cancellation or an exact zero
 //   take the one rare branch);  e = e_big + W - lz;  round to nearest even.
 // --------------------------------------------------------------------------
-template <int L>
+template <int L, bool FW = false>
 __device__ __forceinline__ void mp_add(MP<L>& s, const MP<L>& t) {
   const bool tz = t.is_zero(), sz = s.is_zero();
   // |M_s| < |M_t| matters only for equal exponents: the top limbs decide it.
@@ -456,7 +458,7 @@ __device__ __forceinline__ void mp_add(MP<L>& s, const MP<L>& t) {
     Y[i + 1] = t_big ? s.m[i] : t.m[i];
   }
   uint32_t stk = 0u;
-  shr_bits_sticky<L + 1>(Y, d, stk);
+  shr_bits_sticky<L + 1, FW>(Y, d, stk);
   const uint32_t msk = 0u - sub;
 #pragma unroll
   for (int i = 0; i <= L; ++i) Y[i] ^= msk;

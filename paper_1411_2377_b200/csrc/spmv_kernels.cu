@@ -25,12 +25,16 @@ void launch_counter_add(int64_t k) { g_launches.fetch_add(k); }
 template <int L, int MINB>
 __global__ void __launch_bounds__(128, MINB) spmv_sell(PartView P, XView x, YView y) {
   const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (slot >= P.nslots) return;
+  if (slot >= P.nslots) return;                  // whole warps (nslots = 32 nslices)
   const int row = P.slot_row[slot];
-  if (row < 0) return;
-  const int len = P.slot_len[slot];
   const int l = (int)(slot & 31);
+  // Every lane walks the SLICE's width (its longest row): a shorter row's
+  // padding entries - and a padding slot's - have zero limbs and column 0,
+  // so their products are +0 and RN(s + 0) = s leaves the chain exact.  The
+  // loop is then warp-uniform and the adder's warp collectives take the
+  // full mask (rows in a slice are length-sorted: the padding is small).
   const int64_t g0 = P.slice_ptr[slot >> 5] >> 5;
+  const int len = (int)((P.slice_ptr[(slot >> 5) + 1] >> 5) - g0);
 
   MP<L> s;
   s.set_zero();
@@ -58,7 +62,7 @@ __global__ void __launch_bounds__(128, MINB) spmv_sell(PartView P, XView x, YVie
     if (first) {                     // RN(+0 + t) = t: the first add is a copy
       s = t;                         // (warp-uniform: all lanes are at step j)
     } else {
-      mp_add<L>(s, t);
+      mp_add<L, true>(s, t);
     }
   };
   // columns run two entries ahead of the fetches that use them: a column
@@ -85,7 +89,7 @@ __global__ void __launch_bounds__(128, MINB) spmv_sell(PartView P, XView x, YVie
     }
     step(a1, x1, w1, e1, s1, false);
   }
-  store_y<L>(y, row, s);
+  if (row >= 0) store_y<L>(y, row, s);
 }
 
 // --------------------------------------------------------------------------
