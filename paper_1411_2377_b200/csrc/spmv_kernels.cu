@@ -319,17 +319,13 @@ static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStrea
     }
   }
   // tuning knob (read per launch): MPSP_MINB = min resident blocks per SM
-  // (register cap).  Defaults measured on B200: at L <= 8, 5 (96 registers,
-  // no spills; C4 A x 0.380 -> 0.372 ms, A^T x 0.296 -> 0.279 ms) unless the
-  // whole grid is resident in one wave only at 6 (80 registers, a 28-byte
-  // spill; C2 0.0332 -> 0.0319 ms); 4 at L = 16 (128 registers; C3 0.280 ->
+  // (register cap).  Defaults measured on B200: 6 at L <= 8 (80 registers,
+  // a 12-byte spill; round 1 used 5 unless the grid fitted one wave - since
+  // the warp-uniform slice loop, 6 is faster on C4 A^T x too: 252 vs 256 us,
+  // C4 A x's short rows equal), 4 at L = 16 (128 registers; C3 0.280 ->
   // 0.239 ms); 1 at L = 32 (more spills than gain).
   const char* vm = std::getenv("MPSP_MINB");
-  int minb = L == 16 ? 4 : 1;
-  if (L <= 8) {
-    const int sms = current_sms();
-    minb = (blocks > (int64_t)sms * 5 && blocks <= (int64_t)sms * 6) ? 6 : 5;
-  }
+  int minb = L == 16 ? 4 : (L <= 8 ? 6 : 1);
   if (vm) minb = std::atoi(vm);
   const unsigned nb = (unsigned)blocks;
   switch (minb) {

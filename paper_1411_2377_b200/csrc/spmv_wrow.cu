@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(128, (L <= 8 ? MPSP_WROW_MINB : 1)) spmv_wrow(
         wload<L>(B, x, 32 * (c + 1), valid(c + 1), cn, nxt);
         cn = colof(c + 2);
       }
-      mul_entry<L>(cur.a, cur.w, cur.x, cur.ex, cur.sx, t);
+      mul_entry<L, true>(cur.a, cur.w, cur.x, cur.ex, cur.sx, t);
       ch.consume(t, lane);
     }
   } else {
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(128, (L <= 8 ? MPSP_WROW_MINB : 1)) spmv_wrow(
       WEntry<L> cur;
       wload<L>(B, x, 32 * c, valid(c), cn, cur);
       cn = colof(c + 1);
-      mul_entry<L>(cur.a, cur.w, cur.x, cur.ex, cur.sx, t);
+      mul_entry<L, true>(cur.a, cur.w, cur.x, cur.ex, cur.sx, t);
       ch.consume(t, lane);
     }
   }

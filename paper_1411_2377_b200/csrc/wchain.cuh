@@ -161,7 +161,7 @@ struct WChain {
 #pragma unroll
       for (int i = 0; i < L; ++i) Y[i + 1] = t.m[i];
       uint32_t stk = 0u;
-      shr_bits_sticky<L + 1>(Y, dd, stk);
+      shr_bits_sticky<L + 1, true>(Y, dd, stk);      // the whole warp is here
       const uint32_t rb = Y[0] >> 31;
       const bool sticky = (stk | (Y[0] << 1)) != 0u;
       const bool tie = use && rb && !sticky;
@@ -248,7 +248,7 @@ struct WChain {
 #pragma unroll
     for (int i = 0; i < L; ++i) Y[i + 1] = t.m[i];
     uint32_t stk = 0u;
-    shr_bits_sticky<L + 1>(Y, dd0, stk);
+    shr_bits_sticky<L + 1, true>(Y, dd0, stk);
     {
       const uint32_t fy = Y[0];                     // tau's 32 fraction bits
       const bool fnz = (fy != 0u) || (stk != 0u);   // fraction != 0
@@ -381,7 +381,7 @@ struct WChain {
     for (int i = 0; i < L; ++i) tf.m[i] = __shfl_sync(FULL, t.m[i], f);
     tf.e = __shfl_sync(FULL, t.e, f);
     tf.s = __shfl_sync(FULL, t.s, f);
-    mp_add<L>(s, tf);
+    mp_add<L, true>(s, tf);
     reset_to(s, lane);
   }
 };
