@@ -102,7 +102,7 @@ __device__ __forceinline__ void mul_entry(const uint32_t (&a)[L], int32_t w, con
       return;
     }
   }
-  mp_mul<L>(a, ea, sa, x, ex, sx, t);
+  mp_mul<L, FW>(a, ea, sa, x, ex, sx, t);
 }
 
 template <int L>

@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(128, MINB) spmv_sell(PartView P, XView x, YVie
   auto step = [&](const uint32_t (&a)[L], const uint32_t (&xv)[L], int32_t w, int32_t ex,
                   uint32_t sx, bool first) {
     MP<L> t;
-    mul_entry<L>(a, w, xv, ex, sx, t);
+    mul_entry<L, true>(a, w, xv, ex, sx, t);
     if (first) {                     // RN(+0 + t) = t: the first add is a copy
       s = t;                         // (warp-uniform: all lanes are at step j)
     } else {
