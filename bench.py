@@ -349,7 +349,7 @@ def kernel_names(d, op, L):
     sell = f"spmv_sell_cp<{L}>" if L == 32 and os.environ.get("MPSP_CP", "1") != "0" else f"spmv_sell<{L}>"
     if L > 32:
         return f"spmv_wide<{L // 32}> (warp per row, limbs across lanes)"
-    thr = int(os.environ.get("MPSP_LONG_T", "192"))
+    thr = int(os.environ.get("MPSP_LONG_T", "256"))
     lens = np.diff(d["rowptr"]) if op == "ax" else np.bincount(d["colidx"], minlength=d["n"])
     if int(lens.max(initial=0)) <= thr:
         return sell

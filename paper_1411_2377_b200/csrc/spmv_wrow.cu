@@ -44,7 +44,7 @@ namespace mpsp {
 // (tests lower it to route rows of any length through this kernel).
 int long_row_threshold() {
   const char* v = std::getenv("MPSP_LONG_T");
-  return v ? std::atoi(v) : 192;
+  return v ? std::atoi(v) : 256;
 }
 
 // One step's operands (a_k, x_col) in registers.

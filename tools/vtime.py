@@ -67,8 +67,15 @@ def main():
         handles = []
         for name, L, env in libs:
             h = P()
+            saved = {k: os.environ.get(k) for k in env}
+            os.environ.update(env)             # create-time knobs (MPSP_LONG_T, MPSP_CHUNKS)
             rc = L.mpsp_csr_create(ctypes.byref(h), p, n, *[k.ctypes.data_as(P) for k in keep],
                                    0, n, 1 if op == "atx" else 0)
+            for k, v in saved.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
             assert rc == 0, (name, rc)
             y = (torch.empty(n * Lm, dtype=torch.int32, device=dev), torch.empty(n, dtype=torch.int32, device=dev),
                  torch.empty(n, dtype=torch.uint8, device=dev))
