@@ -34,6 +34,9 @@ struct PartView {
   const uint32_t* limbs;      // [nentries * L]
   int64_t nslots;             // 32 * nslices (SELL part: short rows)
   int64_t nslices;
+  // launch order of the slices (widest first across the row chunks), or
+  // null: the stored order (one chunk, or a chunk view of the host pipeline)
+  const int32_t* slice_order;
   // warp rows (rows longer than the long-row threshold), longest first
   int64_t nwrow;
   const int64_t* wrow_ptr;    // [nwrow] first entry (multiple of 32)

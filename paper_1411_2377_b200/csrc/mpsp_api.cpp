@@ -57,6 +57,7 @@ struct DevPart {
   int64_t* slice_ptr = nullptr;
   int32_t* slot_row = nullptr;
   int32_t* slot_len = nullptr;
+  int32_t* slice_order = nullptr;  // device launch order (null: stored order)
   int64_t* wrow_ptr = nullptr;
   int32_t* wrow_row = nullptr;
   int32_t* wrow_len = nullptr;
@@ -78,6 +79,7 @@ struct DevPart {
     v.slot_len = slot_len + 32 * s0;
     v.nslices = s1 - s0;
     v.nslots = 32 * (s1 - s0);
+    v.slice_order = nullptr;
     v.nwrow = 0;
     return v;
   }
@@ -87,14 +89,15 @@ struct DevPart {
     v.slice_ptr = slice_ptr; v.slot_row = slot_row; v.slot_len = slot_len;
     v.col = col; v.expw = expw; v.limbs = limbs;
     v.nslices = nslices; v.nslots = nslices * 32;
+    v.slice_order = slice_order;
     v.nwrow = nwrow; v.wrow_ptr = wrow_ptr; v.wrow_row = wrow_row; v.wrow_len = wrow_len;
     return v;
   }
   void release() {
-    cudaFree(slice_ptr); cudaFree(slot_row); cudaFree(slot_len);
+    cudaFree(slice_ptr); cudaFree(slot_row); cudaFree(slot_len); cudaFree(slice_order);
     cudaFree(wrow_ptr); cudaFree(wrow_row); cudaFree(wrow_len);
     cudaFree(col); cudaFree(expw); cudaFree(limbs);
-    slice_ptr = nullptr; slot_row = nullptr; slot_len = nullptr;
+    slice_ptr = nullptr; slot_row = nullptr; slot_len = nullptr; slice_order = nullptr;
     wrow_ptr = nullptr; wrow_row = nullptr; wrow_len = nullptr;
     col = nullptr; expw = nullptr; limbs = nullptr;
   }
@@ -314,6 +317,18 @@ int build_part(DevPart& P, int L, int64_t nrows, const int64_t* lrp, const int32
       (rc = up((void**)&P.expw, hexp.data(), hexp.size() * 4)) ||
       (rc = up((void**)&P.limbs, hl.data(), hl.size() * 4)))
     return rc;
+  if (C > 1 && nslices > 1) {
+    // the device entry point launches every chunk's slices at once: widest
+    // first across the chunks, so the longest thread chains start first (in
+    // stored order each chunk's widest slices would start one chunk later;
+    // C3 measured 226 vs 215 us)
+    std::vector<int32_t> ord((size_t)nslices);
+    for (int64_t i = 0; i < nslices; ++i) ord[(size_t)i] = (int32_t)i;
+    std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) {
+      return sp[(size_t)a + 1] - sp[(size_t)a] > sp[(size_t)b + 1] - sp[(size_t)b];
+    });
+    if ((rc = up((void**)&P.slice_order, ord.data(), ord.size() * 4))) return rc;
+  }
   return MPSP_OK;
 }
 

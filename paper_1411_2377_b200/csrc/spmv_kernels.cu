@@ -22,10 +22,18 @@ static std::atomic<int64_t> g_launches{0};
 int64_t launch_counter_get() { return g_launches.load(); }
 void launch_counter_add(int64_t k) { g_launches.fetch_add(k); }
 
+// The slot a thread serves: warp w of the launch takes slice slice_order[w]
+// (widest first across row chunks) when the part has an order, else slice w.
+__device__ __forceinline__ int64_t slot_of(const PartView& P, int64_t gslot) {
+  const int64_t w = gslot >> 5;
+  return (P.slice_order ? (int64_t)__ldg(P.slice_order + w) : w) * 32 + (gslot & 31);
+}
+
 template <int L, int MINB>
 __global__ void __launch_bounds__(128, MINB) spmv_sell(PartView P, XView x, YView y) {
-  const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (slot >= P.nslots) return;                  // whole warps (nslots = 32 nslices)
+  const int64_t gslot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gslot >= P.nslots) return;                 // whole warps (nslots = 32 nslices)
+  const int64_t slot = slot_of(P, gslot);
   const int row = P.slot_row[slot];
   const int l = (int)(slot & 31);
   // Every lane walks the SLICE's width (its longest row): a shorter row's
@@ -123,8 +131,9 @@ __global__ void __launch_bounds__(CP_THREADS, CpMinB<L>::v) spmv_sell_cp(PartVie
   constexpr int NC = L / 4;                      // 16-byte chunks per operand
   extern __shared__ uint4 smc[];                 // [stage][a|x][NC][thread]
   const int tid = threadIdx.x;
-  const int64_t slot = (int64_t)blockIdx.x * blockDim.x + tid;
-  const bool live = slot < P.nslots;
+  const int64_t gslot = (int64_t)blockIdx.x * blockDim.x + tid;
+  const bool live = gslot < P.nslots;
+  const int64_t slot = live ? slot_of(P, gslot) : 0;
   const int row = live ? P.slot_row[slot] : -1;
   if (row < 0) return;
   const int len = P.slot_len[slot];
@@ -212,8 +221,9 @@ __global__ void __launch_bounds__(CP_THREADS, MINB) spmv_sell_cp1(PartView P, XV
   constexpr int NC = L / 4;
   extern __shared__ uint4 smc[];                 // [a|x|s][NC][thread]
   const int tid = threadIdx.x;
-  const int64_t slot = (int64_t)blockIdx.x * blockDim.x + tid;
-  const bool live = slot < P.nslots;
+  const int64_t gslot = (int64_t)blockIdx.x * blockDim.x + tid;
+  const bool live = gslot < P.nslots;
+  const int64_t slot = live ? slot_of(P, gslot) : 0;
   const int row = live ? P.slot_row[slot] : -1;
   if (row < 0) return;
   const int len = P.slot_len[slot];
