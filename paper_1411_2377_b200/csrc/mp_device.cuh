@@ -136,9 +136,11 @@ __device__ __forceinline__ void add3w(uint32_t& a0, uint32_t& a1, uint32_t& a2, 
 // chain depends on the previous one through its 64-bit addend, so a single
 // chain per column serialises the whole product; NCH chains (merged at the
 // end of the column) give the scheduler NCH-way ILP at 3 adds per extra chain.
-// (measured on B200: 2 chains best at L = 16, 32; 1 at L <= 8)
+// (measured on B200: round 1 found 2 chains best at L = 16, 32; with the
+// column-(L-2) short product and the final adder 1 chain is best everywhere:
+// C3 217 -> 214 us, C5 1668 -> 1664 us; 3 chains: 227 / 1751)
 #ifndef MPSP_NCH
-#define MPSP_NCH 2
+#define MPSP_NCH 1
 #endif
 #ifndef MPSP_NCH8
 #define MPSP_NCH8 1
