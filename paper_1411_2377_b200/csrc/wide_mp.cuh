@@ -91,6 +91,13 @@ __device__ __forceinline__ uint32_t wround(uint32_t (&m)[K], uint32_t inc, int l
 // operand).  SHORT: only the columns >= L-3 (others written as 0): the hi
 // columns as above, the three top lo columns from per-lane partial sums over
 // i = j (mod 32) reduced across the warp - the lo MACs (u > v) are skipped.
+// sA: a in the ZERO-GAPPED layout, chunk v (limbs 32v .. 32v+31) at words
+// [64v, 64v + 32) and 32 zero words after it, so the diagonal chunk's skewed
+// reads past the chunk load zeros (no per-MAC select).  The 32 steps of a
+// chunk are unrolled 16x at K = 2, 4 and 8x at K = 8 (measured, C2 at p =
+// 2048 / 4096 / 8192: 4x 1301 / 2917 / 8655 us, 8x 1234 / 2802 / 8509, 16x
+// 1185 / 2763 / 8910, 32x 1762 at p = 2048; before the zero-gapped layout
+// and these unrolls 1456 / 3174 / 8714).
 template <int K, bool SHORT>
 __device__ __forceinline__ void wcolumns(const uint32_t* sA, const uint32_t* sX, uint32_t* cs,
                                          int lane) {
@@ -101,10 +108,10 @@ __device__ __forceinline__ void wcolumns(const uint32_t* sA, const uint32_t* sX,
   for (int u = 0; u < K; ++u) { lo[u] = hi[u] = 0u; lo2[u] = hi2[u] = 0u; }
 #pragma unroll
   for (int v = 0; v < K; ++v) {                    // i in [32v, 32v + 32)
-#pragma unroll 4
+#pragma unroll (K >= 8 ? 8 : 16)
     for (int ii = 0; ii < 32; ++ii) {
       const int i = 32 * v + ii;
-      const uint32_t ai = sA[i];
+      const uint32_t ai = sA[64 * v + ii];
 #pragma unroll
       for (int u = 0; u < K; ++u) {
         const int c = lane + 32 * u;
@@ -116,9 +123,9 @@ __device__ __forceinline__ void wcolumns(const uint32_t* sA, const uint32_t* sX,
           // skewed: lane j takes i2 = 32v + j + 1 + ii, so x[c + L - i2] =
           // x[L - 1 - ii] is one broadcast word; i2 past the chunk (ii >=
           // 31 - j) contributes a zero operand
-          const uint32_t a2 = sA[32 * v + lane + 1 + ii];
+          const uint32_t a2 = sA[64 * v + lane + 1 + ii];   // a zero past the chunk
           const uint32_t x2 = sX[L - 1 - ii];
-          mac64(hi[u], hi2[u], ii < 31 - lane ? a2 : 0u, x2);
+          mac64(hi[u], hi2[u], a2, x2);
         } else {                                   // diagonal chunk: both
           const bool l = ii <= lane;
           const uint32_t xv = sX[l ? c - i : c + L - i];
@@ -134,7 +141,7 @@ __device__ __forceinline__ void wcolumns(const uint32_t* sA, const uint32_t* sX,
 #pragma unroll
     for (int m = 0; m < K; ++m) {
       const int i = lane + 32 * m;
-      const uint32_t ai = sA[i];
+      const uint32_t ai = sA[64 * m + lane];
 #pragma unroll
       for (int r = 0; r < 3; ++r) {
         const int xi = L - 3 + r - i;
@@ -157,6 +164,7 @@ __device__ __forceinline__ void wcolumns(const uint32_t* sA, const uint32_t* sX,
   uint32_t* cs0 = cs;
   uint32_t* cs1 = cs + 2 * L;
   uint32_t* cs2 = cs + 4 * L;
+  __syncwarp();                                    // sA (in cs2's words) fully read
 #pragma unroll
   for (int u = 0; u < K; ++u) {
     const int c = lane + 32 * u;
@@ -231,13 +239,23 @@ __device__ __forceinline__ void wmul(const uint32_t (&a)[K], int32_t ea, uint32_
     wset_zero<K>(t);
     return;
   }
+  // a goes to cs + 4L in the zero-gapped layout of wcolumns (2L words; the
+  // column sums overwrite it at the end of wcolumns); sA is not used
+  uint32_t* sAg = cs + 4 * L;
+  __syncwarp();                                    // a caller's reads of cs are done
+  auto put_a = [&]() {
 #pragma unroll
-  for (int i = 0; i < K; ++i) {
-    sA[lane * K + i] = a[i];
-    sX[lane * K + i] = x[i];
-  }
+    for (int i = 0; i < K; ++i) {
+      const int m = lane * K + i;
+      sAg[64 * (m >> 5) + (m & 31)] = a[i];
+      sAg[64 * (m >> 5) + 32 + (m & 31)] = 0u;
+    }
+  };
+  put_a();
+#pragma unroll
+  for (int i = 0; i < K; ++i) sX[lane * K + i] = x[i];
   __syncwarp();
-  wcolumns<K, true>(sA, sX, cs, lane);
+  wcolumns<K, true>(sAg, sX, cs, lane);
   __syncwarp();
   wcarry<K>(cs, lane);
   const uint32_t* Ps = cs;                         // P (short: limbs >= L-3 valid), 2L words
@@ -248,7 +266,9 @@ __device__ __forceinline__ void wmul(const uint32_t (&a)[K], int32_t ea, uint32_
     const bool amb = ((w1 | w2) == 0u) | ((w1 == 0x00FFFFFFu) & (w2 == wmask));
     if (amb) {                                     // warp-uniform (same smem words): full product
       __syncwarp();
-      wcolumns<K, false>(sA, sX, cs, lane);
+      put_a();                                     // (the column sums overwrote it)
+      __syncwarp();
+      wcolumns<K, false>(sAg, sX, cs, lane);
       __syncwarp();
       wcarry<K>(cs, lane);
       sh = (~Ps[2 * L - 1]) >> 31;

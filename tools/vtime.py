@@ -54,7 +54,8 @@ def main():
     st = torch.cuda.current_stream().cuda_stream
     for c in a.cfgs.split(","):
         cfg, op = (c.split(":") + ["ax"])[:2]
-        d = gen.make(cfg, seed=0)
+        cfg, _, pp = cfg.partition("@")            # "C2@2048": the config at another p
+        d = gen.make(cfg, seed=0, p=int(pp) if pp else None)
         p, n = d["p"], d["n"]
         Lm = p // 32
         hp = lambda arr: np.ascontiguousarray(arr).ctypes.data_as(P)
