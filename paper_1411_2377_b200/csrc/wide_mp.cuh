@@ -149,16 +149,23 @@ __device__ __forceinline__ void wcolumns(const uint32_t* sA, const uint32_t* sX,
         mac64(top[r], top2[r], ai, xi >= 0 ? xv : 0u);
       }
     }
+    // warp sums of the three columns' per-lane partials (top2:top < K 2^64)
+    // by redux.sync on 16-bit pieces: each piece's 32-lane sum is < 2^21, so
+    // the u32 reductions are exact (5 REDUX per column instead of a 5-level
+    // butterfly of three shuffles and a 96-bit add per level)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        const uint64_t po = __shfl_xor_sync(FULL, top[r], o);
-        const uint32_t qo = __shfl_xor_sync(FULL, top2[r], o);
-        const uint64_t sum = top[r] + po;
-        top2[r] += qo + (sum < po ? 1u : 0u);
-        top[r] = sum;
-      }
+    for (int r = 0; r < 3; ++r) {
+      const uint64_t v = top[r];
+      const uint32_t s0 = __reduce_add_sync(FULL, (uint32_t)v & 0xffffu);
+      const uint32_t s1 = __reduce_add_sync(FULL, (uint32_t)v >> 16);
+      const uint32_t s2 = __reduce_add_sync(FULL, (uint32_t)(v >> 32) & 0xffffu);
+      const uint32_t s3 = __reduce_add_sync(FULL, (uint32_t)(v >> 48));
+      const uint32_t t2 = __reduce_add_sync(FULL, top2[r]);
+      const uint64_t A = (uint64_t)s0 + ((uint64_t)s1 << 16);    // < 2^38
+      const uint64_t B = (uint64_t)s2 + ((uint64_t)s3 << 16);    // < 2^38
+      const uint64_t lo64 = A + (B << 32);
+      top[r] = lo64;
+      top2[r] = (uint32_t)(B >> 32) + t2 + (lo64 < A ? 1u : 0u);
     }
   }
   uint32_t* cs0 = cs;

@@ -12,7 +12,7 @@ for s in $SPECS; do
   CMD="python bench.py --config $cfg --op $op --steps 2 --warmup 1 --no-cpu --no-e2e --no-per-config"
   rep=/tmp/prof/prof_${TAG}_${cfg}_${op}_${rx}
   timeout 600 $CMD > gpurun_out/plain_${TAG}_${cfg}_${op}.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$rx -s 1 -c 1 \
+  timeout 900 ncu -f --set full --clock-control none --import-source on -k regex:$rx -s 1 -c 1 \
       -o $rep $CMD > gpurun_out/ncu_${TAG}_${cfg}_${op}_${rx}.log 2>&1
   echo "ncu $s rc=$?"
   if [ -f $rep.ncu-rep ]; then
