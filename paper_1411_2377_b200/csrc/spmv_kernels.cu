@@ -373,9 +373,9 @@ int launch_spmv(int L, const PartView& P, const XView& x, const YView& y, void* 
 //     carry-out on the FMA-heavy pipe + ~0.5 IADD3.X per limb-MAC;
 //   OPERAND scanning: per row a_i * x a carry chain of low words and one of
 //     high words: IMAD + IMAD.HI on the FMA pipes + IADD3.X on the ALU pipe.
-// The peak reported is the faster of the two (B200: operand scanning, ~36 vs
-// ~28 limb-MACs/clk/SM); inside the SpMV kernels operand scanning measured
-// slower (the adder needs the ALU pipe the carries would take), DESIGN.md.
+// The peak reported is the faster of the two (B200, measured: Comba 8.1 T
+// limb-MACs/s = 27.9 per clock per SM, operand scanning 5.65 T - its carry
+// chains keep the ALU pipe busy); DESIGN.md section 5.
 // --------------------------------------------------------------------------
 constexpr int IB_L = 8;
 template <bool OS>

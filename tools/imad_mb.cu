@@ -1,5 +1,9 @@
 // Integer-pipe microbenchmarks (tuning aid): Comba mac3, operand scanning,
 // radix-2^28 64-bit column sums, IMAD.HI, IMAD, IADD+LOP3 throughput.
+// CAUTION: variant B's carry chains are separate NON-volatile asm statements,
+// which the compiler may reorder across the implicit carry flag - its 36
+// MACs/clk/SM is not a valid multi-limb product rate (mpsp_imad_bench keeps
+// the chains in order with asm volatile: 5.65 T vs Comba's 8.1 T limb-MAC/s).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/imad_mb tools/imad_mb.cu
 #include <cstdio>
 #include <cstdint>
