@@ -135,26 +135,26 @@ __device__ __forceinline__ void wcolumns(const uint32_t* sA, const uint32_t* sX,
       }
     }
   }
-  uint64_t top[3] = {0u, 0u, 0u};                  // SHORT: columns L-3, L-2, L-1
-  uint32_t top2[3] = {0u, 0u, 0u};
+  uint64_t top[2] = {0u, 0u};                      // SHORT: columns L-2, L-1
+  uint32_t top2[2] = {0u, 0u};
   if (SHORT) {
 #pragma unroll
     for (int m = 0; m < K; ++m) {
       const int i = lane + 32 * m;
       const uint32_t ai = sA[64 * m + lane];
 #pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        const int xi = L - 3 + r - i;
+      for (int r = 0; r < 2; ++r) {
+        const int xi = L - 2 + r - i;
         const uint32_t xv = sX[xi >= 0 ? xi : 0];
         mac64(top[r], top2[r], ai, xi >= 0 ? xv : 0u);
       }
     }
-    // warp sums of the three columns' per-lane partials (top2:top < K 2^64)
+    // warp sums of the two columns' per-lane partials (top2:top < K 2^64)
     // by redux.sync on 16-bit pieces: each piece's 32-lane sum is < 2^21, so
     // the u32 reductions are exact (5 REDUX per column instead of a 5-level
     // butterfly of three shuffles and a 96-bit add per level)
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
+    for (int r = 0; r < 2; ++r) {
       const uint64_t v = top[r];
       const uint32_t s0 = __reduce_add_sync(FULL, (uint32_t)v & 0xffffu);
       const uint32_t s1 = __reduce_add_sync(FULL, (uint32_t)v >> 16);
@@ -180,10 +180,9 @@ __device__ __forceinline__ void wcolumns(const uint32_t* sA, const uint32_t* sX,
     if (SHORT) {
       lv = 0u;
       l2 = 0u;
-      if (u == K - 1 && lane >= 29) {
-        const int r = lane - 29;
-        lv = r == 0 ? top[0] : (r == 1 ? top[1] : top[2]);
-        l2 = r == 0 ? top2[0] : (r == 1 ? top2[1] : top2[2]);
+      if (u == K - 1 && lane >= 30) {
+        lv = lane == 30 ? top[0] : top[1];
+        l2 = lane == 30 ? top2[0] : top2[1];
       }
     }
     cs0[c] = (uint32_t)lv; cs1[c] = (uint32_t)(lv >> 32); cs2[c] = l2;
@@ -230,10 +229,11 @@ __device__ __forceinline__ void wcarry(uint32_t* cs, int lane) {
 
 // t = RN(a * x).  sA, sX: L words each, cs: 6L words (per-warp shared memory).
 // SHORT PRODUCT with an exactness certificate (the wide form of mp_mul's):
-// only the columns >= K0 = L-3 are formed; the omitted part is
-// N < K0 2^(32(L-2)) (1 + eps) < 2^B, B = 32(L-2) + 8 (K0 < 256), so if the
-// bits between B and the round bit are neither all 0 nor all 1, the rounded
-// product is the exact one's with sticky 1; otherwise (rare) the full product.
+// only the columns >= K0 = L-2 are formed; the omitted part is
+// N < K0 2^(32(L-1)) (1 + eps) < 2^B, B = 32(L-1) + 8 (K0 < 256), so if the
+// 22-23 bits between B and the round bit are neither all 0 nor all 1, the
+// rounded product is the exact one's with sticky 1; otherwise (~2^-21 per
+// random product) the full product.
 template <int K>
 __device__ __forceinline__ void wmul(const uint32_t (&a)[K], int32_t ea, uint32_t sa,
                                      const uint32_t (&x)[K], int32_t ex, uint32_t sx,
@@ -265,12 +265,12 @@ __device__ __forceinline__ void wmul(const uint32_t (&a)[K], int32_t ea, uint32_
   wcolumns<K, true>(sAg, sX, cs, lane);
   __syncwarp();
   wcarry<K>(cs, lane);
-  const uint32_t* Ps = cs;                         // P (short: limbs >= L-3 valid), 2L words
+  const uint32_t* Ps = cs;                         // P (short: limbs >= L-1 valid), 2L words
   uint32_t sh = (~Ps[2 * L - 1]) >> 31;            // top bit clear -> 1
   {
-    const uint32_t wmask = (1u << (31u - sh)) - 1u;
-    const uint32_t w1 = Ps[L - 2] >> 8, w2 = Ps[L - 1] & wmask;
-    const bool amb = ((w1 | w2) == 0u) | ((w1 == 0x00FFFFFFu) & (w2 == wmask));
+    const uint32_t wmask = (1u << (31u - sh)) - 1u;   // Ps[L-1] below the round bit
+    const uint32_t w = (Ps[L - 1] & wmask) >> 8;       // the window, 23 - sh bits
+    const bool amb = (w == 0u) | (w == (wmask >> 8));
     if (amb) {                                     // warp-uniform (same smem words): full product
       __syncwarp();
       put_a();                                     // (the column sums overwrote it)

@@ -55,3 +55,32 @@ def test_wide_row_block():
     rb, re = n // 3, n // 3 + 101
     got = gpu_run(d, "ax", rows=(rb, re))
     assert_same(got, tuple(a[rb:re] for a in full), "row block")
+
+
+@pytest.mark.parametrize("p", [2048, 4096])
+def test_wide_short_product_ambiguous_window(p):
+    """The warp form's certificate window (bits 8 .. 30 - sh of the product's
+    limb L-1: x's bits p-24 .. p-3 when a = 2^(p-1) + 1) all zeros / all
+    ones with nonzero low limbs: every such product takes the full product."""
+    import random
+    rng = random.Random(p)
+    n, per_row = 40, 4
+    xs = []
+    for i in range(n):
+        M = (1 << (p - 1)) | rng.getrandbits(p - 1)
+        win = ((1 << 22) - 1) << (p - 24)
+        M = (M & ~win) | (win if i % 2 else 0) | 1
+        xs.append((rng.getrandbits(1), M, rng.randint(-8, 8)))
+    vals, cols, rowptr = [], [], [0]
+    for r in range(n):
+        for c in sorted(rng.sample(range(n), per_row)):
+            Ma = (1 << (p - 1)) + 1 if rng.random() < 0.7 else (1 << (p - 1)) | rng.getrandbits(p - 1)
+            vals.append((rng.getrandbits(1), Ma, rng.randint(-8, 8)))
+            cols.append(c)
+        rowptr.append(len(cols))
+    al, ae, as_ = gen.pack_triples(vals, p)
+    xl, xe, xsg = gen.pack_triples(xs, p)
+    d = dict(p=p, n=n, rowptr=np.array(rowptr, np.int64), colidx=np.array(cols, np.int32),
+             limbs=al, exps=ae, signs=as_, x_limbs=xl, x_exps=xe, x_signs=xsg)
+    for op in ("ax", "atx"):
+        assert_same(gpu_run(d, op), oracle_full(d, op), f"wide ambiguous window p={p} {op}")

@@ -29,11 +29,12 @@ M32 = (1 << 32) - 1
 def short_product(Ma, Mx, p, D=None):
     """Model of mp_mul: returns (M, dE, certified) or None when the
     certificate fails (the kernel then forms the full product).  Columns
-    k >= K0 = L - D are formed: D = 2 in mp_mul (L <= 32, MPSP_SHORT_D), 3 in
-    the warp form for L = 64..256 (wide_mp.cuh wmul)."""
+    k >= K0 = L - D are formed: D = 2 in mp_mul (L <= 32, MPSP_SHORT_D) and
+    in the warp form for L = 64..256 (wide_mp.cuh wmul); D = 3 models round
+    1's kernels."""
     L = p // 32
     if D is None:
-        D = 2 if L <= 32 else 3
+        D = 2
     a = [(Ma >> (32 * i)) & M32 for i in range(L)]
     x = [(Mx >> (32 * i)) & M32 for i in range(L)]
     K0 = L - D
@@ -45,8 +46,9 @@ def short_product(Ma, Mx, p, D=None):
     assert 0 <= N < (1 << B)                      # the bound the certificate uses
     sh = 0 if (T >> (64 * L - 1)) & 1 else 1
     rpos = 32 * L - 1 - sh                        # round bit position
-    if D == 2:
-        B += 1 - sh                               # the kernel's window: bits 6..30 of T[1] << sh
+    if D == 2 and L <= 32:
+        B += 1 - sh                               # mp_mul's window: bits 6..30 of T[1] << sh
+    # (wmul's window at D = 2: bits 8 .. 30-sh of limb L-1, i.e. [B, rpos))
     W = (T >> B) & ((1 << (rpos - B)) - 1)
     if W == 0 or W == (1 << (rpos - B)) - 1:
         return None
@@ -60,8 +62,8 @@ def short_product(Ma, Mx, p, D=None):
     return q, dE
 
 
-@pytest.mark.parametrize("p,D", [(128, 2), (256, 2), (512, 2), (1024, 2), (256, 3), (1024, 3),
-                                 (2048, 3), (8192, 3)])
+@pytest.mark.parametrize("p,D", [(128, 2), (256, 2), (512, 2), (1024, 2), (2048, 2), (8192, 2),
+                                 (256, 3), (1024, 3), (2048, 3), (8192, 3)])
 def test_short_product_certificate_random(p, D):
     rng = random.Random(p)
     hits = 0
@@ -77,7 +79,7 @@ def test_short_product_certificate_random(p, D):
     assert hits == (3000 if p <= 1024 else 300)   # random mantissas never need the full product
 
 
-@pytest.mark.parametrize("p,D", [(128, 2), (256, 2), (512, 2), (256, 3), (2048, 3)])
+@pytest.mark.parametrize("p,D", [(128, 2), (256, 2), (512, 2), (2048, 2), (256, 3), (2048, 3)])
 def test_short_product_certificate_adversarial(p, D):
     """Structured mantissas (powers of two, all-ones runs, carries rippling
     into the round bit, exact ties): whenever the certificate passes the
