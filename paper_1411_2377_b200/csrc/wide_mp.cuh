@@ -363,9 +363,15 @@ __device__ __forceinline__ void wadd(WMP<K>& s, const WMP<K>& t, uint32_t* ys, i
       y[i] = __funnelshift_r(ys[k + q], ys[k + q + 1], r);
     }
     if (lane == 0) yg = __funnelshift_r(ys[q], ys[q + 1], r);
-    uint32_t orr = 0u;                               // bits below the guard limb
-    for (uint32_t k = lane; k < q; k += 32) orr |= ys[k];
-    if (lane == 0) orr |= ys[q] & ((1u << r) - 1u);
+    // bits below the guard limb: ys[0 .. q) and ys[q]'s low r bits, i.e. the
+    // small operand's limbs 0 .. q-2 and limb q-1's low r bits - read from
+    // the registers of the lanes that hold them
+    uint32_t orr = 0u;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const uint32_t m1 = (uint32_t)(lane * K + i) + 1u;   // ys position of limb lane*K+i
+      orr |= m1 < q ? Y[i] : (m1 == q ? (Y[i] & ((1u << r) - 1u)) : 0u);
+    }
     stk0 = __ballot_sync(FULL, orr != 0u) != 0u ? 1u : 0u;
     __syncwarp();                                    // ys reads done
   }
