@@ -280,7 +280,8 @@ int mpsp_gpbicg(mpsp_csr *A,
 
 /* Diagnostics of the segmented dot: out[0] = segments the
  * chain warp evaluated step by step, out[1] = segments committed from their
- * speculative sums, since the last call (counters are then reset). */
+ * speculative sums, since the last call (counters are then reset); the
+ * p <= 1024 and p > 1024 chains' counts are summed. */
 int mpsp_debug_dot_stats(unsigned long long out[2]);
 
 /*

@@ -323,7 +323,29 @@ __global__ void __launch_bounds__(32 * KW) wdot_products(int64_t n, VecIn u, Vec
 //      (RN(S u + t_k) = (S + Q_k) u: no tie, no binade change), so S += R;
 //      any other segment is walked step by step with wadd from the stored
 //      products.  The result is the ordered chain's, bit for bit.
-constexpr int WSEG = 64;
+#ifndef MPSP_WSEG
+#define MPSP_WSEG 64
+#endif
+#ifndef MPSP_WSUB
+#define MPSP_WSUB 16
+#endif
+constexpr int WSEG = MPSP_WSEG;
+// Lower levels: a segment that fails validation is retried as WSEG / WSUB
+// sub-segments with their own speculation records (guessed from the fp64
+// prefix at each sub-segment start), a failing sub-segment as WSUB / WSUB2
+// third-level segments, and only those that fail are walked element by
+// element (BiCG at p = 2048: 17% of the 64-element segments failed, and
+// their walks dominated the solve).  Measured, BiCG / GPBiCG per iteration
+// at p = 2048 (n = 84,617): one level 28.9 / 91.8 ms; (64, 16) 20.5 / 63.2;
+// (64, 16, 4) 19.9 / 60.0; (64, 16, 8) 19.2 / 58.0; (64, 16, 2) 30.1 / 75.6;
+// (64, 8) 22.3 / 60.5; (128, 16) 20.0 / 63.4; (128, 32) 22.9 / 74.1.
+constexpr int WSUB = MPSP_WSUB;
+#ifndef MPSP_WSUB2
+#define MPSP_WSUB2 8
+#endif
+constexpr int WSUB2 = MPSP_WSUB2;                 // third level (0: none)
+static_assert(WSEG % WSUB == 0, "sub-segments tile a segment");
+static_assert(WSUB2 == 0 || WSUB % WSUB2 == 0, "third-level segments tile a sub-segment");
 
 template <int K>
 struct WSeg {
@@ -339,14 +361,15 @@ struct WSeg {
 };
 
 template <int K>
-__global__ void __launch_bounds__(128) wseg_sums(int64_t n, int64_t nseg, WSeg<K> G, const int* stop) {
+__global__ void __launch_bounds__(128) wseg_sums(int64_t n, int64_t nseg, int seglen, WSeg<K> G,
+                                                 const int* stop) {
   if (stop && *stop) return;
   const int64_t seg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (seg >= nseg) return;
   double acc = 0.0;
-  for (int j = lane; j < WSEG; j += 32) {
-    const int64_t k = seg * WSEG + j;
+  for (int j = lane; j < seglen; j += 32) {
+    const int64_t k = seg * seglen + j;
     if (k < n) acc += G.fp[k];
   }
 #pragma unroll
@@ -379,8 +402,8 @@ __device__ __forceinline__ void wi_store(uint32_t* g, const uint32_t (&a)[W], in
 }
 
 template <int K>
-__global__ void __launch_bounds__(32 * KW) wseg_speculate(int64_t n, int64_t nseg, VecIn P, WSeg<K> G,
-                                                          const int* stop) {
+__global__ void __launch_bounds__(32 * KW) wseg_speculate(int64_t n, int64_t nseg, int seglen, VecIn P,
+                                                          WSeg<K> G, const int* stop) {
   constexpr int L = 32 * K, W = K + 1, PB = 32 * L;
   if (stop && *stop) return;
   extern __shared__ uint32_t wsm[];
@@ -397,8 +420,8 @@ __global__ void __launch_bounds__(32 * KW) wseg_speculate(int64_t n, int64_t nse
   uint32_t R[W], mn[W], mx[W];
 #pragma unroll
   for (int i = 0; i < W; ++i) { R[i] = 0u; mn[i] = 0u; mx[i] = 0u; }
-  for (int j = 0; j < WSEG && valid; ++j) {
-    const int64_t k = seg * WSEG + j;
+  for (int j = 0; j < seglen && valid; ++j) {
+    const int64_t k = seg * seglen + j;
     if (k >= n) break;
     WMP<K> t;
     wload<K>(P, k, lane, t);
@@ -456,9 +479,13 @@ __global__ void __launch_bounds__(32 * KW) wseg_speculate(int64_t n, int64_t nse
   wi_store<W>(G.mx + seg * 32 * W, mx, lane);
 }
 
+// diagnostics: segments walked element by element / committed (added to
+// mpsp_debug_dot_stats' counters)
+__device__ unsigned long long g_wdot_stats[2];
+
 template <int K>
 __global__ void __launch_bounds__(32) wseg_chain(int64_t n, int64_t nseg, VecIn P, WSeg<K> G,
-                                                 YView out, const int* stop) {
+                                                 WSeg<K> Gs, WSeg<K> Gt, YView out, const int* stop) {
   constexpr int L = 32 * K, W = K + 1;
   if (stop && *stop) return;
   extern __shared__ uint32_t wsm[];
@@ -472,40 +499,62 @@ __global__ void __launch_bounds__(32) wseg_chain(int64_t n, int64_t nseg, VecIn 
   }
   WMP<K> s;
   wset_zero<K>(s);
-  for (int64_t seg = 0; seg < nseg; ++seg) {
-    bool ok = seg > 0 && G.valid[seg] && !wzero<K>(s) && G.eg[seg] == s.e && G.sg[seg] == s.s;
+  // commit segment j of the records R if its guess and bounds hold for the
+  // exact state s (then every step was S += Q_k on the grid: S += ds)
+  auto try_commit = [&](const WSeg<K>& R, int64_t j) -> bool {
+    bool ok = j > 0 && R.valid[j] && !wzero<K>(s) && R.eg[j] == s.e && R.sg[j] == s.s;
+    if (lane == 0) atomicAdd(&g_wdot_stats[ok ? 1 : 0], 1ull);
+    if (!ok) return false;
     uint32_t S[W];
-    if (ok) {
-      to_wi<K, W>(s.m, S, wsm, lane);
-      uint32_t A[W], B[W], M[W];
-      wi_load<W>(G.mn + seg * 32 * W, M, lane);
+    to_wi<K, W>(s.m, S, wsm, lane);
+    uint32_t A[W], B[W], M[W];
+    wi_load<W>(R.mn + j * 32 * W, M, lane);
 #pragma unroll
-      for (int i = 0; i < W; ++i) A[i] = S[i];
-      wi_add<W>(A, M, lane);
-      wi_load<W>(G.mx + seg * 32 * W, M, lane);
+    for (int i = 0; i < W; ++i) A[i] = S[i];
+    wi_add<W>(A, M, lane);
+    wi_load<W>(R.mx + j * 32 * W, M, lane);
 #pragma unroll
-      for (int i = 0; i < W; ++i) B[i] = S[i];
-      wi_add<W>(B, M, lane);
-      ok = !wi_slt<W>(A, LO, lane) && !wi_slt<W>(HI, B, lane);
+    for (int i = 0; i < W; ++i) B[i] = S[i];
+    wi_add<W>(B, M, lane);
+    if (wi_slt<W>(A, LO, lane) || wi_slt<W>(HI, B, lane)) return false;   // warp-uniform
+    uint32_t D[W];
+    wi_load<W>(R.ds + j * 32 * W, D, lane);
+    wi_add<W>(S, D, lane);
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < W; ++i) wsm[lane * W + i] = S[i];
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < K; ++i) s.m[i] = wsm[lane * K + i];
+    __syncwarp();
+    return true;
+  };
+  auto walk = [&](int64_t k0, int64_t k1) {
+    WMP<K> t;
+    for (int64_t k = k0; k < k1; ++k) {
+      wload<K>(P, k, lane, t);
+      wadd<K>(s, t, wsm, lane);
+      __syncwarp();
     }
-    if (ok) {
-      uint32_t D[W];
-      wi_load<W>(G.ds + seg * 32 * W, D, lane);
-      wi_add<W>(S, D, lane);
-      __syncwarp();
-#pragma unroll
-      for (int i = 0; i < W; ++i) wsm[lane * W + i] = S[i];
-      __syncwarp();
-#pragma unroll
-      for (int i = 0; i < K; ++i) s.m[i] = wsm[lane * K + i];
-      __syncwarp();
-    } else {
-      const int64_t k1 = min(n, (seg + 1) * WSEG);
-      WMP<K> t;
-      for (int64_t k = seg * WSEG; k < k1; ++k) {
-        wload<K>(P, k, lane, t);
-        wadd<K>(s, t, wsm, lane);
-        __syncwarp();
+  };
+  constexpr int NSUB = WSEG / WSUB;
+  for (int64_t seg = 0; seg < nseg; ++seg) {
+    if (try_commit(G, seg)) continue;
+    for (int u = 0; u < NSUB; ++u) {               // the segment's sub-segments
+      const int64_t j = seg * NSUB + u;
+      const int64_t k0 = j * WSUB;
+      if (k0 >= n) break;
+      if (try_commit(Gs, j)) continue;
+      if constexpr (WSUB2 > 0) {
+        constexpr int NSUB2 = WSUB / (WSUB2 > 0 ? WSUB2 : 1);
+        for (int v = 0; v < NSUB2; ++v) {          // and theirs
+          const int64_t jj = j * NSUB2 + v;
+          const int64_t kk = jj * WSUB2;
+          if (kk >= n) break;
+          if (!try_commit(Gt, jj)) walk(kk, min(n, kk + WSUB2));
+        }
+      } else {
+        walk(k0, min(n, k0 + WSUB));
       }
     }
   }
@@ -678,45 +727,67 @@ struct WideOps {
   static int attr(Kern k, size_t bytes) {
     return (int)cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   }
+  static size_t rec_bytes(size_t nseg) {          // one level's speculation records
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    constexpr int W = K + 1;
+    return al(nseg * 8) + 3 * al(nseg * 4) + 3 * al(nseg * 32 * W * 4);
+  }
   static size_t bytes(int64_t n) {
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-    const size_t nseg = (size_t)((n + WSEG - 1) / WSEG);
-    constexpr int W = K + 1;
+    const size_t nseg = (size_t)((n + WSEG - 1) / WSEG), nsub = (size_t)((n + WSUB - 1) / WSUB);
+    const size_t nsub2 = WSUB2 > 0 ? (size_t)((n + WSUB2 - 1) / WSUB2) : 1;
     return al((size_t)n * L * 4) + al((size_t)n * 4) + al((size_t)n) + al((size_t)n * 8) +
-           al(nseg * 8) + 3 * al(nseg * 4) + 3 * al(nseg * 32 * W * 4);
+           rec_bytes(nseg) + rec_bytes(nsub) + rec_bytes(nsub2);
+  }
+  // carve one level's records out of p
+  static WSeg<K> records(char*& p, double* fp, size_t nseg) {
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    constexpr int W = K + 1;
+    WSeg<K> G;
+    G.fp = fp;
+    G.segsum = (double*)p; p += al(nseg * 8);
+    G.valid = (int32_t*)p; p += al(nseg * 4);
+    G.eg = (int32_t*)p; p += al(nseg * 4);
+    G.sg = (uint32_t*)p; p += al(nseg * 4);
+    G.ds = (uint32_t*)p; p += al(nseg * 32 * W * 4);
+    G.mn = (uint32_t*)p; p += al(nseg * 32 * W * 4);
+    G.mx = (uint32_t*)p; p += al(nseg * 32 * W * 4);
+    return G;
   }
   static int dot(int64_t n, VecIn u, VecIn v, YView out, const int* stop, cudaStream_t st, void* work) {
     if (!work && n > 0) return (int)cudaErrorInvalidValue;
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-    constexpr int W = K + 1;
-    const int64_t nseg = (n + WSEG - 1) / WSEG;
+    const int64_t nseg = (n + WSEG - 1) / WSEG, nsub = (n + WSUB - 1) / WSUB;
+    const int64_t nsub2 = WSUB2 > 0 ? (n + WSUB2 - 1) / WSUB2 : 1;
     char* p = (char*)work;
     YView P{(uint32_t*)p, (int32_t*)(p + al((size_t)n * L * 4)),
             (uint8_t*)(p + al((size_t)n * L * 4) + al((size_t)n * 4))};
     p += al((size_t)n * L * 4) + al((size_t)n * 4) + al((size_t)n);
-    WSeg<K> G;
-    G.fp = (double*)p; p += al((size_t)n * 8);
-    G.segsum = (double*)p; p += al((size_t)nseg * 8);
-    G.valid = (int32_t*)p; p += al((size_t)nseg * 4);
-    G.eg = (int32_t*)p; p += al((size_t)nseg * 4);
-    G.sg = (uint32_t*)p; p += al((size_t)nseg * 4);
-    G.ds = (uint32_t*)p; p += al((size_t)nseg * 32 * W * 4);
-    G.mn = (uint32_t*)p; p += al((size_t)nseg * 32 * W * 4);
-    G.mx = (uint32_t*)p;
+    double* fp = (double*)p;
+    p += al((size_t)n * 8);
+    const WSeg<K> G = records(p, fp, (size_t)nseg);
+    const WSeg<K> Gs = records(p, fp, (size_t)nsub);
+    const WSeg<K> Gt = records(p, fp, (size_t)nsub2);
     const VecIn Pin{P.limbs, P.exps, P.signs};
     int e;
     if (n > 0) {
       if ((e = attr(wdot_products<K>, KW * SM))) return e;
       const int64_t blocks = std::min<int64_t>((n + KW - 1) / KW, 148 * 16);
-      wdot_products<K><<<(unsigned)blocks, 32 * KW, KW * SM, st>>>(n, u, v, P, G.fp, stop);
-      wseg_sums<K><<<(unsigned)((nseg * 32 + 127) / 128), 128, 0, st>>>(n, nseg, G, stop);
-      if ((e = launch_dot_prefix(G.segsum, nseg, stop, st))) return e;
+      wdot_products<K><<<(unsigned)blocks, 32 * KW, KW * SM, st>>>(n, u, v, P, fp, stop);
       if ((e = attr(wseg_speculate<K>, KW * SM))) return e;
-      wseg_speculate<K><<<(unsigned)((nseg + KW - 1) / KW), 32 * KW, KW * SM, st>>>(n, nseg, Pin, G, stop);
-      launch_counter_add(3);
+      for (int lev = 0; lev < (WSUB2 > 0 ? 3 : 2); ++lev) {   // the segment levels
+        const WSeg<K>& R = lev == 0 ? G : (lev == 1 ? Gs : Gt);
+        const int64_t ns = lev == 0 ? nseg : (lev == 1 ? nsub : nsub2);
+        const int len = lev == 0 ? WSEG : (lev == 1 ? WSUB : WSUB2);
+        wseg_sums<K><<<(unsigned)((ns * 32 + 127) / 128), 128, 0, st>>>(n, ns, len, R, stop);
+        if ((e = launch_dot_prefix(R.segsum, ns, stop, st))) return e;
+        wseg_speculate<K><<<(unsigned)((ns + KW - 1) / KW), 32 * KW, KW * SM, st>>>(n, ns, len, Pin, R,
+                                                                                stop);
+      }
+      launch_counter_add(WSUB2 > 0 ? 7 : 5);
     }
     if ((e = attr(wseg_chain<K>, SM))) return e;
-    wseg_chain<K><<<1, 32, SM, st>>>(n, nseg, Pin, G, out, stop);
+    wseg_chain<K><<<1, 32, SM, st>>>(n, nseg, Pin, G, Gs, Gt, out, stop);
     launch_counter_add(1);
     return (int)cudaGetLastError();
   }
@@ -779,6 +850,17 @@ int krylov_wide_scalar(int L, const YView& S, int* fl, int op, void* stream) {
     case 256: return wide::WideOps<8>::scalar(S, fl, op, st);
     default: return (int)cudaErrorInvalidValue;
   }
+}
+
+// [walked, committed] segments of the p > 1024 dot chain since the last
+// call (then reset); mpsp_debug_dot_stats adds them to the narrow chain's
+int krylov_wide_dot_stats(unsigned long long out[2]) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, wide::g_wdot_stats, sizeof(unsigned long long) * 2);
+  if (e == cudaSuccess) {
+    const unsigned long long z[2] = {0ull, 0ull};
+    e = cudaMemcpyToSymbol(wide::g_wdot_stats, z, sizeof z);
+  }
+  return (int)e;
 }
 
 }  // namespace mpsp

@@ -82,6 +82,7 @@ int krylov_dot(int L, int64_t n, const VecIn& u, const VecIn& v, const YView& ou
                void* stream, void* work);   // work: krylov_dot_work_bytes, or null (one warp)
 size_t krylov_dot_work_bytes(int L, int64_t n);
 int krylov_dot_stats(unsigned long long out[2]);   // [sequential, validated] segments, reset
+int krylov_wide_dot_stats(unsigned long long out[2]);   // the same for p > 1024
 // exclusive fp64 prefix of per-segment sums, in place (one 1024-thread block)
 int launch_dot_prefix(double* segsum, int64_t nseg, const int* stop, void* stream);
 int krylov_axpy(int L, int64_t n, const VecIn& al, int neg, const VecIn& x, const VecIn& y,

@@ -1285,8 +1285,14 @@ int mpsp_gpbicg(mpsp_csr* A, const uint32_t* b_limbs, const int32_t* b_exps, con
 
 int mpsp_debug_dot_stats(unsigned long long out[2]) {
   if (!out) return MPSP_E_ARG;
-  const int e = krylov_dot_stats(out);
-  return e ? cuda_fail((cudaError_t)e) : MPSP_OK;
+  int e = krylov_dot_stats(out);
+  if (e) return cuda_fail((cudaError_t)e);
+  unsigned long long w[2] = {0ull, 0ull};
+  e = krylov_wide_dot_stats(w);
+  if (e) return cuda_fail((cudaError_t)e);
+  out[0] += w[0];
+  out[1] += w[1];
+  return MPSP_OK;
 }
 
 int mpsp_imad_bench(double out[5]) {
