@@ -502,23 +502,28 @@ __global__ void __launch_bounds__(32) wseg_chain(int64_t n, int64_t nseg, VecIn 
   // commit segment j of the records R if its guess and bounds hold for the
   // exact state s (then every step was S += Q_k on the grid: S += ds)
   auto try_commit = [&](const WSeg<K>& R, int64_t j) -> bool {
-    bool ok = j > 0 && R.valid[j] && !wzero<K>(s) && R.eg[j] == s.e && R.sg[j] == s.s;
+    // every load of the record issued up front: one memory latency on the
+    // lone chain warp's path instead of four
+    const int vj = R.valid[j];
+    const int32_t egj = R.eg[j];
+    const uint32_t sgj = R.sg[j];
+    uint32_t Mn[W], Mx[W], D[W];
+    wi_load<W>(R.mn + j * 32 * W, Mn, lane);
+    wi_load<W>(R.mx + j * 32 * W, Mx, lane);
+    wi_load<W>(R.ds + j * 32 * W, D, lane);
+    bool ok = j > 0 && vj && !wzero<K>(s) && egj == s.e && sgj == s.s;
     if (lane == 0) atomicAdd(&g_wdot_stats[ok ? 1 : 0], 1ull);
     if (!ok) return false;
     uint32_t S[W];
     to_wi<K, W>(s.m, S, wsm, lane);
-    uint32_t A[W], B[W], M[W];
-    wi_load<W>(R.mn + j * 32 * W, M, lane);
+    uint32_t A[W], B[W];
 #pragma unroll
     for (int i = 0; i < W; ++i) A[i] = S[i];
-    wi_add<W>(A, M, lane);
-    wi_load<W>(R.mx + j * 32 * W, M, lane);
+    wi_add<W>(A, Mn, lane);
 #pragma unroll
     for (int i = 0; i < W; ++i) B[i] = S[i];
-    wi_add<W>(B, M, lane);
+    wi_add<W>(B, Mx, lane);
     if (wi_slt<W>(A, LO, lane) || wi_slt<W>(HI, B, lane)) return false;   // warp-uniform
-    uint32_t D[W];
-    wi_load<W>(R.ds + j * 32 * W, D, lane);
     wi_add<W>(S, D, lane);
     __syncwarp();
 #pragma unroll
