@@ -501,16 +501,31 @@ __global__ void __launch_bounds__(32) wseg_chain(int64_t n, int64_t nseg, VecIn 
   wset_zero<K>(s);
   // commit segment j of the records R if its guess and bounds hold for the
   // exact state s (then every step was S += Q_k on the grid: S += ds)
-  auto try_commit = [&](const WSeg<K>& R, int64_t j) -> bool {
-    // every load of the record issued up front: one memory latency on the
-    // lone chain warp's path instead of four
-    const int vj = R.valid[j];
-    const int32_t egj = R.eg[j];
-    const uint32_t sgj = R.sg[j];
+  // one segment's speculation record, loaded with every load issued up
+  // front (one memory latency on the lone chain warp's path instead of four)
+  struct Rec {
+    int v;
+    int32_t eg;
+    uint32_t sg;
     uint32_t Mn[W], Mx[W], D[W];
-    wi_load<W>(R.mn + j * 32 * W, Mn, lane);
-    wi_load<W>(R.mx + j * 32 * W, Mx, lane);
-    wi_load<W>(R.ds + j * 32 * W, D, lane);
+  };
+  auto load_rec = [&](const WSeg<K>& R, int64_t j, Rec& r) {
+    r.v = R.valid[j];
+    r.eg = R.eg[j];
+    r.sg = R.sg[j];
+    wi_load<W>(R.mn + j * 32 * W, r.Mn, lane);
+    wi_load<W>(R.mx + j * 32 * W, r.Mx, lane);
+    wi_load<W>(R.ds + j * 32 * W, r.D, lane);
+  };
+  auto commit_rec = [&](const Rec& r, int64_t j) -> bool {
+    const int vj = r.v;
+    const int32_t egj = r.eg;
+    const uint32_t sgj = r.sg;
+    const uint32_t(&Mn)[W] = r.Mn;
+    const uint32_t(&Mx)[W] = r.Mx;
+    uint32_t D[W];
+#pragma unroll
+    for (int i = 0; i < W; ++i) D[i] = r.D[i];
     bool ok = j > 0 && vj && !wzero<K>(s) && egj == s.e && sgj == s.s;
     if (lane == 0) atomicAdd(&g_wdot_stats[ok ? 1 : 0], 1ull);
     if (!ok) return false;
@@ -534,6 +549,11 @@ __global__ void __launch_bounds__(32) wseg_chain(int64_t n, int64_t nseg, VecIn 
     __syncwarp();
     return true;
   };
+  auto try_commit = [&](const WSeg<K>& R, int64_t j) -> bool {
+    Rec r;
+    load_rec(R, j, r);
+    return commit_rec(r, j);
+  };
   auto walk = [&](int64_t k0, int64_t k1) {
     WMP<K> t;
     for (int64_t k = k0; k < k1; ++k) {
@@ -543,8 +563,13 @@ __global__ void __launch_bounds__(32) wseg_chain(int64_t n, int64_t nseg, VecIn 
     }
   };
   constexpr int NSUB = WSEG / WSUB;
+  Rec cur, nxt;
+  if (nseg > 0) load_rec(G, 0, cur);
   for (int64_t seg = 0; seg < nseg; ++seg) {
-    if (try_commit(G, seg)) continue;
+    if (seg + 1 < nseg) load_rec(G, seg + 1, nxt);  // in flight during this segment
+    const bool done = commit_rec(cur, seg);
+    cur = nxt;
+    if (done) continue;
     for (int u = 0; u < NSUB; ++u) {               // the segment's sub-segments
       const int64_t j = seg * NSUB + u;
       const int64_t k0 = j * WSUB;
