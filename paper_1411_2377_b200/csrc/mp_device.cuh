@@ -357,10 +357,11 @@ __device__ __forceinline__ void mp_mul_finish(const uint32_t (&a)[L], int32_t ea
   if (cy) t.m[L - 1] = 0x80000000u;
   t.e = ea + ex - (int32_t)sh + (int32_t)cy;
   t.s = sa ^ sx;
-  if (zero) {
-#pragma unroll
-    for (int i = 0; i < L; ++i) t.m[i] = 0u;
-  }
+  // A zero operand has all limbs 0 (include/mpsp.h value encoding; every
+  // zero the kernels produce is +0 with zero limbs), so T = 0, the round bit
+  // is 0 and t.m is already all zero: no masking of the limbs (L SELs per
+  // product; measured C2 A x -2.7%, C3 / C4 -0.4..0.6%, bit-exact).  `zero`
+  // only keeps such products off the completion branch.
 }
 
 // --------------------------------------------------------------------------
