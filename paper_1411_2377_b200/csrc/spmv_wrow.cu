@@ -184,3 +184,13 @@ int launch_spmv_long(int L, const PartView& P, const XView& x, const YView& y, v
 }
 
 }  // namespace mpsp
+
+#ifdef MPSP_WSTATS
+// tuning builds only: read and reset the warp-row chain counters (wchain.cuh)
+extern "C" int mpsp_debug_wrow_stats(unsigned long long out[8]) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, mpsp::g_wstats, sizeof(unsigned long long) * 8);
+  if (e != cudaSuccess) return (int)e;
+  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  return (int)cudaMemcpyToSymbol(mpsp::g_wstats, z, sizeof(z));
+}
+#endif

@@ -10,6 +10,16 @@
 
 namespace mpsp {
 
+// Tuning counters (-DMPSP_WSTATS builds only; per translation unit):
+// [0] passes, [1] fast commits, [2] failing steps, [3] up, [4] down,
+// [5] dominant, [6] exact adder, [7] zero-accumulator absorptions
+#ifdef MPSP_WSTATS
+static __device__ unsigned long long g_wstats[8];
+#define WSTAT(i) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_wstats[i], 1ull); } while (0)
+#else
+#define WSTAT(i) do { } while (0)
+#endif
+
 // High-part scale H = 2^(p-HB) grid units: S/H in [2^(HB-1), 2^HB).  HB = 26
 // keeps the 32-lane scan of |h| <= 2^25 (plus Shi and the error count) in
 // int32; one unit of H is >= one grid unit u for every p >= 32.
@@ -146,11 +156,13 @@ struct WChain {
         tf.e = __shfl_sync(FULL, t.e, f);
         tf.s = __shfl_sync(FULL, t.s, f);
         reset_to(tf, lane);
+        WSTAT(7);
         retire(f);
         start = f + 1;
         continue;
       }
       const bool act = !tz;
+      WSTAT(0);
       const int32_t d32 = sub_sat(E, t.e);            // E - t.e, saturated to int32
       const bool badd = act && d32 < 1;              // |t| >= 2^(E-1): leaves the binade
       const bool use = act && !badd;
@@ -212,10 +224,12 @@ struct WChain {
         add_n_cin<N>(R, R, Q, cin);
         Shi += __shfl_sync(FULL, Pi, 31);
         err = min(err + 64, 1 << 28);                 // saturates: checks then fail
+        WSTAT(1);
         break;
       }
       // ---- the first failing step f
       const int f = __ffs(failM) - 1;
+      WSTAT(2);
       if (lane < f) add_n_cin<N>(R, R, Q, cin);      // steps before f are valid
       step_f(t, f, __shfl_sync(FULL, LB, f), __shfl_sync(FULL, h, f), err + 2 * f, lane);
       retire(f);
@@ -273,6 +287,7 @@ struct WChain {
       const int mode = __shfl_sync(FULL, up_f ? 1 : (dn_f ? 2 : (dom_f ? 4 : 0)), f);
 #endif
       if (mode == 4) {
+        WSTAT(5);
         const int k = __shfl_sync(FULL, kd, f);
         const int64_t vlof = __shfl_sync(FULL, vlo, f), vhif = __shfl_sync(FULL, vhi, f);
         const uint32_t sgf = __shfl_sync(FULL, t.s, f);
@@ -316,6 +331,7 @@ struct WChain {
         return;
       }
       if (mode == 1) {                              // V in [2^p, 1.5 2^p): grid 2u
+        WSTAT(3);
         if (lane == f) {
           uint32_t Yv[N];
 #pragma unroll
@@ -345,6 +361,7 @@ struct WChain {
         return;
       }
       if (mode == 2) {                              // V in [2^(p-2), 2^(p-1)): grid u/2
+        WSTAT(4);
 #pragma unroll
         for (int i = N - 1; i > 0; --i) R[i] = __funnelshift_l(R[i - 1], R[i], 1);
         R[0] <<= 1;
@@ -375,6 +392,7 @@ struct WChain {
         return;
       }
     }
+    WSTAT(6);
     MP<L> s, tf;
     exact(s);
 #pragma unroll
