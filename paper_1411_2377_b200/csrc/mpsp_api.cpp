@@ -777,17 +777,34 @@ static int spmv_host(mpsp_csr* A, bool transpose, const uint32_t* xl, const int3
   }
   XView xv{(const uint32_t*)dx[0], (const int32_t*)dx[1], (const uint8_t*)dx[2]};
   YView yv{(uint32_t*)dy[0], (int32_t*)dy[1], (uint8_t*)dy[2]};
-  int64_t copied = 0, xneed = 0;
+  int64_t copied = 0, scopied = 0, xneed = 0;
   const size_t esz[3] = {(size_t)L * 4, 4, 1};
+  // MPSP_E2E_SMALL (default 1): the exponent and sign arrays (1/(4L+5) of the
+  // bytes) move in few copies - x's for the first chunk's window, then the
+  // rest at the second chunk, y's after the last chunk - instead of two small
+  // DMA transfers per chunk and direction; 0 keeps them per chunk.
+  const char* vb = std::getenv("MPSP_E2E_SMALL");
+  const bool batch = !(vb && vb[0] == '0');
+  auto h2d = [&](int i, int64_t lo, int64_t hi) -> cudaError_t {
+    if (hi <= lo) return cudaSuccess;
+    return cudaMemcpyAsync((char*)dx[i] + lo * esz[i], (const char*)xp[i] + lo * esz[i],
+                           (size_t)(hi - lo) * esz[i], cudaMemcpyHostToDevice, A->s_h2d);
+  };
+  void* hy[3] = {yl, ye, ys};
+  auto d2h = [&](int i, int64_t lo, int64_t hi) -> cudaError_t {
+    if (hi <= lo) return cudaSuccess;
+    return cudaMemcpyAsync((char*)hy[i] + lo * esz[i], (const char*)dy[i] + lo * esz[i],
+                           (size_t)(hi - lo) * esz[i], cudaMemcpyDeviceToHost, A->s_d2h);
+  };
   for (int64_t c = 0; c < C; ++c) {
     xneed = std::min<int64_t>(n, std::max<int64_t>(xneed, P.chi[(size_t)c]));
-    if (xneed > copied) {
-      for (int i = 0; i < 3; ++i)
-        if ((e = cudaMemcpyAsync((char*)dx[i] + copied * esz[i], (const char*)xp[i] + copied * esz[i],
-                                 (size_t)(xneed - copied) * esz[i], cudaMemcpyHostToDevice, A->s_h2d)) != cudaSuccess)
-          return cuda_fail(e);
-      copied = xneed;
-    }
+    if ((e = h2d(0, copied, xneed)) != cudaSuccess) return cuda_fail(e);
+    copied = std::max(copied, xneed);
+    // small arrays: the first chunk's window, then the rest of x at once
+    const int64_t sneed = (batch && c > 0) ? n : xneed;
+    for (int i = 1; i < 3; ++i)
+      if ((e = h2d(i, scopied, sneed)) != cudaSuccess) return cuda_fail(e);
+    scopied = std::max(scopied, sneed);
     if ((e = cudaEventRecord(A->ev_x[(size_t)c], A->s_h2d)) != cudaSuccess) return cuda_fail(e);
     if ((e = cudaStreamWaitEvent(A->stream, A->ev_x[(size_t)c], 0)) != cudaSuccess) return cuda_fail(e);
     const int err = launch_spmv(L, P.chunk_view((int)c), xv, yv, A->stream);
@@ -795,11 +812,13 @@ static int spmv_host(mpsp_csr* A, bool transpose, const uint32_t* xl, const int3
     if ((e = cudaEventRecord(A->ev_y[(size_t)c], A->stream)) != cudaSuccess) return cuda_fail(e);
     if ((e = cudaStreamWaitEvent(A->s_d2h, A->ev_y[(size_t)c], 0)) != cudaSuccess) return cuda_fail(e);
     const int64_t r0 = P.crow[(size_t)c], r1 = P.crow[(size_t)c + 1];
-    void* hy[3] = {yl, ye, ys};
-    for (int i = 0; i < 3; ++i)
-      if (r1 > r0 && (e = cudaMemcpyAsync((char*)hy[i] + r0 * esz[i], (const char*)dy[i] + r0 * esz[i],
-                                          (size_t)(r1 - r0) * esz[i], cudaMemcpyDeviceToHost, A->s_d2h)) != cudaSuccess)
-        return cuda_fail(e);
+    for (int i = 0; i < 3; ++i) {
+      if (batch && i > 0) {
+        if (c == C - 1 && (e = d2h(i, 0, r)) != cudaSuccess) return cuda_fail(e);
+        continue;
+      }
+      if ((e = d2h(i, r0, r1)) != cudaSuccess) return cuda_fail(e);
+    }
   }
   if ((e = cudaStreamSynchronize(A->s_d2h)) != cudaSuccess) return cuda_fail(e);
   if ((e = cudaStreamSynchronize(A->stream)) != cudaSuccess) return cuda_fail(e);

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--cfg", default="C5")
     ap.add_argument("--chunks", default="8,16,32")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--small", default="0,1", help="MPSP_E2E_SMALL values to time")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -74,11 +75,15 @@ def main():
         ye = torch.empty((n,), dtype=torch.int32).pin_memory()
         ys = torch.empty((n,), dtype=torch.uint8).pin_memory()
         hy = (yl.numpy().view(np.uint32), ye.numpy(), ys.numpy())
-        ms = wall(lambda: A.spmv_host(*hx, out=hy))
-        if first is None:
-            first = tuple(v.copy() for v in hy)
-        same = all(np.array_equal(u, v) for u, v in zip(first, hy))
-        print(f"  MPSP_CHUNKS={c}: spmv_host {ms:.2f} ms  same_as_first={same}", flush=True)
+        for small in a.small.split(","):
+            os.environ["MPSP_E2E_SMALL"] = small       # read per call
+            hy[0][:] = 0
+            ms = wall(lambda: A.spmv_host(*hx, out=hy))
+            if first is None:
+                first = tuple(v.copy() for v in hy)
+            same = all(np.array_equal(u, v) for u, v in zip(first, hy))
+            print(f"  MPSP_CHUNKS={c} MPSP_E2E_SMALL={small}: spmv_host {ms:.2f} ms  "
+                  f"same_as_first={same}", flush=True)
         A.close()
 
 
