@@ -336,17 +336,21 @@ def test_interior_boundary_split_emulated(cfg, n, op):
             assert n_inner > n // 2            # banded / stencil blocks are mostly interior
 
 
+@pytest.mark.parametrize("small", ["1", "0"])
 @pytest.mark.parametrize("chunks", ["1", "3", "7"])
 @pytest.mark.parametrize("cfg,n,op", [("C5", 4900, "ax"), ("C3", 3000, "ax"), ("C2", 5000, "atx"),
                                       ("C1", 700, "ax"), ("C4", 4000, "atx")])
-def test_row_chunks_device_and_host_pipeline(cfg, n, op, chunks, monkeypatch):
+def test_row_chunks_device_and_host_pipeline(cfg, n, op, chunks, small, monkeypatch):
     """Row-chunked layout (rows length-sorted within C contiguous chunks,
     env MPSP_CHUNKS forcing C on small matrices) and the host-buffer
     pipeline of mpsp_spmv_host (per chunk: H2D of x up to the chunk's window
-    end, the chunk's kernels, D2H of its y rows, on three streams) - both
-    bit-exact against the oracle, from pinned and pageable host buffers."""
+    end, the chunk's kernels, D2H of its y rows, on three streams; the
+    exponent / sign arrays batched (MPSP_E2E_SMALL=1, default) or per chunk)
+    - both bit-exact against the oracle, from pinned and pageable host
+    buffers."""
     import torch
     monkeypatch.setenv("MPSP_CHUNKS", chunks)
+    monkeypatch.setenv("MPSP_E2E_SMALL", small)
     d = gen.make(cfg, n=n, seed=31)
     want = oracle_full(d, op)
     A = _csr(d, transpose=(op == "atx"))
