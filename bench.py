@@ -601,7 +601,8 @@ def main():
         rec = json.load(open(tj)).get(workload_name(args))
         if rec:
             roof["traffic"] = rec["traffic_bytes"]
-            src = rec["summary"] or f"profiles/{rec['report']}"
+            src = rec["summary"] or rec["report"]
+            src = src if src.startswith("profiles/") else f"profiles/{src}"
             roof["traffic_source"] = f"{src} ({rec['kernel']})"
     roof["kernel"] = kernel_names(d, args.op, L)
     roof["frac_of_t_roof"] = roof["t_roof_ms"] / roof["kernel_ms"]
