@@ -32,8 +32,9 @@ arithmetic with a single rounding, hand-worked examples and brute force.
 ``spmv``/``spmv_t`` are pinned by the invariants listed in DESIGN.md (identity,
 permutation, transpose, small-integer exactness, scaling, negation,
 densification) and by the 1-nnz-row == single rounding property.  The paper
-prints no SpMV values, so whole-config outputs are "parity unpinned by the
-paper" (pinned only through the pieces above).  ``dense_mv`` (the paper's
+prints no SpMV values to store as a fixture: whole-config outputs are pinned
+through the pieces above and the hand-worked SpMV examples of tests/golden/
+(every function of this module has a pin).  ``dense_mv`` (the paper's
 section-3 dense MP MV) is pinned by closed forms (Lotkin
 row 1 times [1..n] = n(n+1)/2 exactly; A e_j = column j) and by dense ==
 sparse bitwise (tests/test_lotkin.py).  Every function works at any p that is
