@@ -210,6 +210,21 @@ __global__ void __launch_bounds__(CP_THREADS, CpMinB<L>::v) spmv_sell_cp(PartVie
   store_y<L>(y, row, s);
 }
 
+// tuning knobs of the one-stage kernel: threads per block / resident blocks
+// per SM (shared memory 12L x threads bytes per block bounds the product)
+#ifndef MPSP_CP1_T
+#define MPSP_CP1_T 32
+#endif
+#ifndef MPSP_CP1_B
+#define MPSP_CP1_B 16
+#endif
+#ifndef MPSP_CP1_L16
+#define MPSP_CP1_L16 0      // 1: L = 16 takes the one-stage kernel too (experiment)
+#endif
+#ifndef MPSP_CP1_B16
+#define MPSP_CP1_B16 16
+#endif
+constexpr int CP1_THREADS = MPSP_CP1_T;
 // spmv_sell_cp1<L>: the same with ONE stage per operand (12 KB of shared
 // memory per warp instead of 16: 4 blocks of 128 threads fit an SM): entry
 // j+1's copies are issued once entry j's product has consumed the slots (the
@@ -217,7 +232,12 @@ __global__ void __launch_bounds__(CP_THREADS, CpMinB<L>::v) spmv_sell_cp(PartVie
 // entry j and the other warps' work; the accumulator is parked in its own
 // region during the product.
 template <int L, int MINB>
-__global__ void __launch_bounds__(CP_THREADS, MINB) spmv_sell_cp1(PartView P, XView x, YView y) {
+#ifdef MPSP_CP1_MAXREG
+__global__ void __maxnreg__(MPSP_CP1_MAXREG) spmv_sell_cp1(
+#else
+__global__ void __launch_bounds__(CP1_THREADS, MINB) spmv_sell_cp1(
+#endif
+    PartView P, XView x, YView y) {
   constexpr int NC = L / 4;
   extern __shared__ uint4 smc[];                 // [a|x|s][NC][thread]
   const int tid = threadIdx.x;
@@ -233,9 +253,9 @@ __global__ void __launch_bounds__(CP_THREADS, MINB) spmv_sell_cp1(PartView P, XV
   const int32_t* expp = P.expw + g0 * 32 + l;
   const uint4* A4 = reinterpret_cast<const uint4*>(P.limbs);
   const uint4* X4 = reinterpret_cast<const uint4*>(x.limbs);
-  auto sa = [&](int c) { return smc + (0 * NC + c) * CP_THREADS + tid; };
-  auto sx = [&](int c) { return smc + (1 * NC + c) * CP_THREADS + tid; };
-  auto ss = [&](int c) { return smc + (2 * NC + c) * CP_THREADS + tid; };
+  auto sa = [&](int c) { return smc + (0 * NC + c) * CP1_THREADS + tid; };
+  auto sx = [&](int c) { return smc + (1 * NC + c) * CP1_THREADS + tid; };
+  auto ss = [&](int c) { return smc + (2 * NC + c) * CP1_THREADS + tid; };
   int32_t wq = 0, exq = 0;
   uint32_t sq = 0u;
   auto issue = [&](int j, int col) {
@@ -308,7 +328,8 @@ static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStrea
   if (nshort <= 0) return 0;
   const int threads = 128;
   const int64_t blocks = (nshort + threads - 1) / threads;
-  if constexpr (L == 32) {
+  if constexpr (L == 32 || (L == 16 && MPSP_CP1_L16)) {
+    constexpr int B1 = L == 32 ? MPSP_CP1_B : MPSP_CP1_B16;
     const char* vc = std::getenv("MPSP_CP");       // 0: register-prefetch kernel, 2: two stages
     if (!(vc && vc[0] == '0')) {
       constexpr int NC = L / 4;
@@ -320,10 +341,11 @@ static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStrea
         g_launches.fetch_add(1);
         return (int)cudaGetLastError();
       }
-      const size_t smem = (size_t)3 * NC * CP_THREADS * 16;     // a, x, parked s: 12L KB
+      const size_t smem = (size_t)3 * NC * CP1_THREADS * 16;    // a, x, parked s: 12L KB at 128 threads
+      const int64_t blocks1 = (nshort + CP1_THREADS - 1) / CP1_THREADS;
       static std::atomic<uint64_t> attr1{0};
-      if (int e = ensure_smem_attr((const void*)spmv_sell_cp1<L, 4>, smem, attr1)) return e;
-      spmv_sell_cp1<L, 4><<<(unsigned)blocks, CP_THREADS, smem, st>>>(P, x, y);
+      if (int e = ensure_smem_attr((const void*)spmv_sell_cp1<L, B1>, smem, attr1)) return e;
+      spmv_sell_cp1<L, B1><<<(unsigned)blocks1, CP1_THREADS, smem, st>>>(P, x, y);
       g_launches.fetch_add(1);
       return (int)cudaGetLastError();
     }
