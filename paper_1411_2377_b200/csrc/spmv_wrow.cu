@@ -94,6 +94,11 @@ __device__ __forceinline__ void wload(const WRowBase<L>& B, const XView& x, int 
 #ifndef MPSP_WROW_MINB
 #define MPSP_WROW_MINB 4
 #endif
+// threads per block (the warps of a block never cooperate: the block size
+// only sets the granularity at which an SM's warp slots refill)
+#ifndef MPSP_WROW_T
+#define MPSP_WROW_T 128
+#endif
 // ---------------------------------------------------------------------------
 // spmv_wrow<L>: one warp per row; per block of 32 steps each lane forms the
 // product of its step and the chain advances by WChain::consume.  Operands
@@ -102,7 +107,7 @@ __device__ __forceinline__ void wload(const WRowBase<L>& B, const XView& x, int 
 // itself - no index array is read.
 // ---------------------------------------------------------------------------
 template <int L, bool DENSE = false>
-__global__ void __launch_bounds__(128, (L <= 8 ? MPSP_WROW_MINB : 1)) spmv_wrow(PartView P, XView x, YView y) {
+__global__ void __launch_bounds__(MPSP_WROW_T, (L <= 8 ? MPSP_WROW_MINB * (128 / MPSP_WROW_T) : 1)) spmv_wrow(PartView P, XView x, YView y) {
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= P.nwrow) return;
@@ -159,7 +164,7 @@ static int launch_wrow_L(const PartView& P, const XView& x, const YView& y, cuda
                          bool dense) {
   const int64_t nw = P.nwrow;
   if (nw <= 0) return 0;
-  const int threads = 128;
+  const int threads = MPSP_WROW_T;
   const int64_t blocks = (nw * 32 + threads - 1) / threads;
   if (dense)
     spmv_wrow<L, true><<<(unsigned)blocks, threads, 0, st>>>(P, x, y);
