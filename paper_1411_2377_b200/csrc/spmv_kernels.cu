@@ -29,8 +29,14 @@ __device__ __forceinline__ int64_t slot_of(const PartView& P, int64_t gslot) {
   return (P.slice_order ? (int64_t)__ldg(P.slice_order + w) : w) * 32 + (gslot & 31);
 }
 
+// threads per block (build knob; MINB counts blocks of 128 threads per SM -
+// the threads never cooperate, the block size only sets the granularity at
+// which an SM's slots refill)
+#ifndef MPSP_SELL_T
+#define MPSP_SELL_T 128
+#endif
 template <int L, int MINB>
-__global__ void __launch_bounds__(128, MINB) spmv_sell(PartView P, XView x, YView y) {
+__global__ void __launch_bounds__(MPSP_SELL_T, (MINB * 128 / MPSP_SELL_T)) spmv_sell(PartView P, XView x, YView y) {
   const int64_t gslot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gslot >= P.nslots) return;                 // whole warps (nslots = 32 nslices)
   const int64_t slot = slot_of(P, gslot);
@@ -326,7 +332,7 @@ template <int L>
 static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStream_t st) {
   const int64_t nshort = P.nslots;
   if (nshort <= 0) return 0;
-  const int threads = 128;
+  const int threads = MPSP_SELL_T;
   const int64_t blocks = (nshort + threads - 1) / threads;
   if constexpr (L == 32 || (L == 16 && MPSP_CP1_L16)) {
     constexpr int B1 = L == 32 ? MPSP_CP1_B : MPSP_CP1_B16;
@@ -337,7 +343,7 @@ static int launch_L(const PartView& P, const XView& x, const YView& y, cudaStrea
         const size_t smem = (size_t)4 * NC * CP_THREADS * 16;   // 2 stages x (a, x): 16L KB
         static std::atomic<uint64_t> attr{0};
         if (int e = ensure_smem_attr((const void*)spmv_sell_cp<L>, smem, attr)) return e;
-        spmv_sell_cp<L><<<(unsigned)blocks, CP_THREADS, smem, st>>>(P, x, y);
+        spmv_sell_cp<L><<<(unsigned)((nshort + CP_THREADS - 1) / CP_THREADS), CP_THREADS, smem, st>>>(P, x, y);
         g_launches.fetch_add(1);
         return (int)cudaGetLastError();
       }
